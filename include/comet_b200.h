@@ -1,0 +1,143 @@
+/*
+ * comet_b200.h -- C ABI of the B200-native fused MoE layer (COMET,
+ * arxiv 2502.19811) behind the reference package's layer API.
+ *
+ * The reference (`moepipe`, /root/reference/pkg/src/moepipe) is pure Python;
+ * its "FFI" for this path is the Python function boundary
+ *   execute_scheduled / execute_naive / execute_tp_sharded  (executor.py:132-246)
+ * fed by resolve_layer0 / resolve_layer1 / sort_tokens_by_source
+ *   (resolver.py:171-309) and the block split of select_split
+ *   (assigner.py:260-292, simulator.py:45-65).
+ * Each entry point below names the reference interface it replaces.  The
+ * Python mirror (paper_2502_19811_b200/_lib.py) binds these with ctypes;
+ * INTEGRATION.md shows the binding a maintainer adds to moepipe.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; device pointers are CUDA device memory
+ *     owned by the caller unless stated; `stream` is a cudaStream_t.
+ *   - every call is asynchronous on `stream` unless it says it synchronises.
+ *   - return 0 on success; non-zero => comet_last_error() has the message
+ *     (the Python layer raises ConfigurationError for COMET_EINVAL, the
+ *     reference's error type, config.py:16-17).
+ *   - a context is not re-entrant; one host thread per context.
+ */
+#ifndef COMET_B200_H_
+#define COMET_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COMET_OK 0
+#define COMET_EINVAL 1   /* bad shape / config / schedule -> ConfigurationError */
+#define COMET_ECUDA 2    /* CUDA runtime / driver failure */
+#define COMET_ECAP 3     /* index capacity exceeded */
+
+/* Activation between the two expert GEMMs (executor.py:86-90 hook). */
+#define COMET_ACT_IDENTITY 0
+#define COMET_ACT_RELU 1
+#define COMET_ACT_SILU 2
+#define COMET_ACT_GELU_TANH 3
+#define COMET_ACT_TANH 4
+
+typedef struct comet_ctx comet_ctx;
+
+/* Shape + sharding of one rank.  Mirrors ModelConfig / ParallelSpec
+ * (config.py:23-128); m_cap bounds the global token count M per call. */
+typedef struct comet_config {
+  int rank, world, tp, ep, device;
+  int E, topk, N, K; /* full K; each rank holds K / tp */
+  int m_cap;
+} comet_config;
+
+/* Flat view of one rank's routing index (host copies made by
+ * comet_index_download).  Field meaning follows the reference objects:
+ *   counts          RoutingTable.expert_counts          routing.py:78-84
+ *   transfer        RoutingTable.transfer_counts        routing.py:106-117
+ *   row_off/token/src  sort_tokens_by_source layout     resolver.py:171-195
+ *   tiles0          resolve_layer0 tiles (expert,row_start,row_stop,n_deps)
+ *                                                       resolver.py:206-252
+ *   tiles1, chunks  resolve_layer1 tiles (expert,row_start,row_stop,
+ *                   col_start,col_stop,n_deps) and reduce chunks
+ *                   (col_start,col_stop,first_tile,n_tiles) resolver.py:255-309
+ * Arrays are caller-allocated with the capacities returned by
+ * comet_index_sizes. */
+typedef struct comet_index_host {
+  int32_t meta[16];
+  int32_t *counts, *transfer, *row_off, *n_local, *row_token, *row_src;
+  int32_t *tiles0, *tiles1, *chunks;
+  int32_t *pairs0, *pull_token, *pull_src;
+} comet_index_host;
+
+const char* comet_last_error(void);
+int comet_version(void);
+
+int comet_ctx_create(const comet_config* cfg, comet_ctx** out);
+int comet_ctx_destroy(comet_ctx* ctx);
+
+/* Symmetric heap (the paper's NVSHMEM buffer, buffer_bytes = dtype*M*N,
+ * config.py:218-226): token-slot buffer + combine buffer + flags, same
+ * size and offsets on every rank.  export writes a 64-byte CUDA IPC handle;
+ * import takes world*64 bytes gathered from all ranks (torch.distributed
+ * all_gather at init) and maps every peer over NVLink. */
+int comet_symm_export(comet_ctx* ctx, void* handle64);
+int comet_symm_import(comet_ctx* ctx, const void* handles);
+/* In-process group (several ranks emulated on one device, or one process
+ * driving several devices with peer access): link the contexts directly. */
+int comet_link_local(comet_ctx** ctxs, int n);
+
+/* Device pointer to this rank's token-slot buffer [m_cap, N] bf16: the
+ * caller places its own tokens at rows [start_r, stop_r) before forward. */
+void* comet_token_buffer(comet_ctx* ctx);
+/* Device pointer to the [m_cap * topk] int32 routing buffer used by forward. */
+void* comet_routing_buffer(comet_ctx* ctx);
+
+/* moe_index_build for this rank from the global router output
+ * d_experts[M, topk] (int32, ascending per token).  tile_rows / tile_cols
+ * are the reference SharedTensorMeta knobs for the emitted tile lists
+ * (resolver.py:32-96); the kernels always run 128-row tiles in 2-CTA pairs.
+ * Bumps the context epoch (one forward = one epoch). */
+int comet_index_build(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_rows, int tile_cols,
+                      void* stream);
+/* Sizes of the index arrays after a build (synchronises the stream). */
+int comet_index_sizes(comet_ctx* ctx, int32_t meta_out[16], void* stream);
+/* Copy the index to host arrays (synchronises the stream). */
+int comet_index_download(comet_ctx* ctx, comet_index_host* out, void* stream);
+
+/* Publish "this rank's tokens are in its token buffer" to every peer. */
+int comet_signal_tokens_ready(comet_ctx* ctx, void* stream);
+
+/* layer0: NVLink dispatch (n_comm CTAs) fused with GroupGEMM FC1 +
+ * activation.  w0t: [E_r, K/tp, N] bf16 (the rank's experts, K-major).
+ * n_comm: communication CTAs (even, >= 0); group: pairs per L2 group. */
+int comet_layer0(comet_ctx* ctx, const void* w0t, int activation, int n_comm, int group, void* stream);
+
+/* layer1: GroupGEMM FC2 fused with the top-k (weighted) reduce and the
+ * combine to source ranks.  w1t: [E_r, N, K/tp] bf16.  combine_w: global
+ * [M, topk] fp32 (device) or NULL.  y_local: [M_r, N] bf16 output of this
+ * rank's tokens.  n_comm >= 2, even; wave: n-blocks per column wave. */
+int comet_layer1(comet_ctx* ctx, const void* w1t, const float* combine_w, void* y_local, int n_comm,
+                 int wave, void* stream);
+
+/* Whole layer forward of one rank: index build, token-ready signal,
+ * layer0, layer1 (+ remote combine finish when world > 1). */
+int comet_forward(comet_ctx* ctx, const int32_t* d_experts, int M, const void* w0t, const void* w1t,
+                  const float* combine_w, void* y_local, int activation, int n_comm0, int n_comm1,
+                  int group0, int wave1, void* stream);
+
+/* Device pointers of internal buffers (testing / profiling). */
+void* comet_hidden_buffer(comet_ctx* ctx);   /* H [rows_pad_cap, K/tp] bf16 */
+void* comet_yrows_buffer(comet_ctx* ctx);    /* layer1 rows [rows_pad_cap, N] bf16 */
+int32_t comet_hidden_rows_cap(comet_ctx* ctx);
+
+/* Number of SMs and max co-resident 2-CTA clusters for the layer kernel. */
+int comet_device_info(int device, int32_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COMET_B200_H_ */

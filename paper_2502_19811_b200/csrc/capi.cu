@@ -1,0 +1,612 @@
+// C ABI (include/comet_b200.h): context, symmetric heap, launchers.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comet_b200.h"
+#include "index.cuh"
+#include "layers.cuh"
+
+namespace comet {
+__global__ void index_build_kernel(IndexDev ix);
+__global__ void moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                                 const __grid_constant__ CUtensorMap tm_out, const LayerArgs p);
+__global__ void combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb, const uint32_t* cb_flag,
+                                      const int32_t* experts);
+__global__ void signal_x_ready_kernel(uint32_t* const* x_ready_peer, int rank, int world, uint32_t epoch);
+}  // namespace comet
+
+using namespace comet;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) return fail(COMET_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                   \
+  } while (0)
+
+constexpr int kLayerThreads = 256;
+constexpr int kLayerStages = 6;
+constexpr size_t kLayerSmem = kLayerStages * 32768 + 2 * 16384 + 1024 + 256;
+constexpr int kIndexThreads = 1024;
+constexpr size_t kIndexSmem = 8192 * sizeof(long long);
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D bf16 row-major [rows, cols] map, 128-byte swizzle, box {64, box_rows}.
+int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(COMET_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((cols * 2) % 16 != 0) return fail(COMET_EINVAL, "row pitch %llu B not 16-byte aligned", (unsigned long long)(cols * 2));
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COMET_ECUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu", (int)r,
+                                     (unsigned long long)rows, (unsigned long long)cols);
+  return COMET_OK;
+}
+
+struct MapCache {
+  const void* ptr = nullptr;
+  uint64_t rows = 0, cols = 0;
+  CUtensorMap map;
+};
+
+}  // namespace
+
+struct comet_ctx {
+  comet_config cfg;
+  int e_lo = 0, E_r = 0, k_local = 0, n_sm = 0, max_clusters = 0;
+  int nb0 = 0, nb1 = 0, kb0 = 0, kb1 = 0;
+  uint32_t epoch = 0;
+  int M = 0;  // tokens of the current forward
+
+  // index
+  IndexDev ix{};
+  void* index_mem = nullptr;
+  size_t index_bytes = 0;
+  int cap_rows = 0, cap_rows_pad = 0, cap_tiles0 = 0, cap_tiles1 = 0, cap_pairs = 0;
+  int32_t* tiles_mem = nullptr;  // tiles0 + tiles1 + chunks (re-sized by tile knobs)
+  int cap_chunks = 0;
+
+  // symmetric region
+  void* symm = nullptr;
+  size_t symm_bytes = 0;
+  __nv_bfloat16* xs = nullptr;
+  uint32_t* tok_ready = nullptr;
+  uint32_t* x_ready = nullptr;
+  __nv_bfloat16* cb = nullptr;
+  uint32_t* cb_flag = nullptr;
+  int mloc_cap = 0;
+  std::vector<void*> opened;  // IPC-mapped peer bases
+
+  // device peer tables: [xs_peer | cb_peer | cb_flag_peer | x_ready_peer] x world
+  void** peer_tab = nullptr;
+
+  // work buffers
+  __nv_bfloat16* H = nullptr;
+  __nv_bfloat16* yrows = nullptr;
+  uint32_t* counters = nullptr;  // nb_done[nb1] | nb_sent[nb1]
+  int32_t* routing = nullptr;
+
+  CUtensorMap tm_xs, tm_H, tm_y;
+  MapCache w0c, w1c;
+};
+
+extern "C" {
+
+const char* comet_last_error(void) { return g_err.c_str(); }
+int comet_version(void) { return 1; }
+
+int comet_device_info(int device, int32_t out[4]) {
+  CK(cudaSetDevice(device));
+  int n_sm = 0, major = 0, minor = 0;
+  CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  CK(cudaFuncSetAttribute(moe_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLayerSmem));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(n_sm);
+  lc.blockDim = dim3(kLayerThreads);
+  lc.dynamicSmemBytes = kLayerSmem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int clusters = 0;
+  CK(cudaOccupancyMaxActiveClusters(&clusters, moe_layer_kernel, &lc));
+  out[0] = n_sm;
+  out[1] = clusters;
+  out[2] = major * 10 + minor;
+  out[3] = (int)kLayerSmem;
+  return COMET_OK;
+}
+
+int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
+  const comet_config& c = *cfg;
+  if (c.world != c.tp * c.ep || c.world < 1 || c.world > kMaxWorld)
+    return fail(COMET_EINVAL, "world=%d must equal tp*ep=%d and be in [1, %d]", c.world, c.tp * c.ep, kMaxWorld);
+  if (c.rank < 0 || c.rank >= c.world) return fail(COMET_EINVAL, "rank %d out of range", c.rank);
+  if (c.E % c.ep) return fail(COMET_EINVAL, "E=%d is not divisible by ep=%d", c.E, c.ep);
+  if (c.K % c.tp) return fail(COMET_EINVAL, "K=%d is not divisible by tp=%d", c.K, c.tp);
+  if (c.E > 1024) return fail(COMET_EINVAL, "E=%d > 1024 unsupported", c.E);
+  if (c.topk < 1 || c.topk > c.E) return fail(COMET_EINVAL, "bad topk %d", c.topk);
+  if (c.m_cap < 1) return fail(COMET_EINVAL, "m_cap must be >= 1");
+
+  comet_ctx* x = new comet_ctx();
+  x->cfg = c;
+  CK(cudaSetDevice(c.device));
+  int32_t info[4];
+  if (int rc = comet_device_info(c.device, info)) { delete x; return rc; }
+  x->n_sm = info[0];
+  x->max_clusters = info[1];
+  x->E_r = c.E / c.ep;
+  x->e_lo = (c.rank / c.tp) * x->E_r;
+  x->k_local = c.K / c.tp;
+  x->nb0 = (x->k_local + kBlockN - 1) / kBlockN;
+  x->nb1 = (c.N + kBlockN - 1) / kBlockN;
+  x->kb0 = c.N / 64;
+  x->kb1 = x->k_local / 64;
+
+  // ---- index arrays ----
+  const long long rows = (long long)c.m_cap * std::min(c.topk, x->E_r);
+  x->cap_rows = (int)rows;
+  x->cap_rows_pad = (int)align_up(rows + (long long)x->E_r * (kPairRows - 1), kPairRows);
+  x->cap_pairs = x->cap_rows_pad / kPairRows;
+  const int W = c.world;
+  struct Part { int32_t** dst; size_t n; };
+  IndexDev& ix = x->ix;
+  std::vector<Part> parts = {
+      {&ix.counts, (size_t)c.E},
+      {&ix.transfer, (size_t)W * W},
+      {&ix.row_off, (size_t)x->E_r + 1},
+      {&ix.pad_off, (size_t)x->E_r + 1},
+      {&ix.n_local, (size_t)x->E_r},
+      {&ix.row_token, (size_t)x->cap_rows},
+      {&ix.row_src, (size_t)x->cap_rows},
+      {&ix.gather_row, (size_t)x->cap_rows_pad},
+      {&ix.tok_pos, (size_t)c.m_cap * c.topk},
+      {&ix.pairs0, (size_t)x->cap_pairs * 4},
+      {&ix.pairs1, (size_t)x->cap_pairs * 4},
+      {&ix.pull_token, (size_t)c.m_cap},
+      {&ix.pull_src, (size_t)c.m_cap},
+      {&ix.combine_tok, (size_t)c.m_cap},
+      {&ix.meta, (size_t)kMetaSlots},
+      {&ix.first_key, (size_t)c.m_cap},
+      {&ix.key_slot, (size_t)x->cap_rows_pad},
+      {&ix.pair_key, (size_t)x->cap_pairs},
+  };
+  size_t total = 0;
+  for (auto& p : parts) total += align_up(p.n * 4, 256);
+  total += 256;  // done counter
+  CK(cudaMalloc(&x->index_mem, total));
+  CK(cudaMemset(x->index_mem, 0, total));
+  x->index_bytes = total;
+  {
+    char* b = static_cast<char*>(x->index_mem);
+    for (auto& p : parts) {
+      *p.dst = reinterpret_cast<int32_t*>(b);
+      b += align_up(p.n * 4, 256);
+    }
+    ix.done = reinterpret_cast<uint32_t*>(b);
+  }
+  ix.cap_rows = x->cap_rows;
+  ix.cap_rows_pad = x->cap_rows_pad;
+  ix.cap_pairs = x->cap_pairs;
+
+  // ---- symmetric region ----
+  x->mloc_cap = c.m_cap / W + W;
+  const size_t xs_b = align_up((size_t)c.m_cap * c.N * 2, 4096);
+  const size_t tr_b = align_up((size_t)c.m_cap * 4, 4096);
+  const size_t xr_b = 4096;
+  const size_t cb_b = align_up((size_t)W * x->mloc_cap * c.N * 2, 4096);
+  const size_t cf_b = align_up((size_t)W * x->nb1 * 4, 4096);
+  x->symm_bytes = xs_b + tr_b + xr_b + cb_b + cf_b;
+  CK(cudaMalloc(&x->symm, x->symm_bytes));
+  CK(cudaMemset(x->symm, 0, x->symm_bytes));
+  {
+    char* b = static_cast<char*>(x->symm);
+    x->xs = reinterpret_cast<__nv_bfloat16*>(b);
+    b += xs_b;
+    x->tok_ready = reinterpret_cast<uint32_t*>(b);
+    b += tr_b;
+    x->x_ready = reinterpret_cast<uint32_t*>(b);
+    b += xr_b;
+    x->cb = reinterpret_cast<__nv_bfloat16*>(b);
+    b += cb_b;
+    x->cb_flag = reinterpret_cast<uint32_t*>(b);
+  }
+  CK(cudaMalloc(&x->peer_tab, sizeof(void*) * 4 * W));
+  x->opened.assign(W, nullptr);
+
+  // ---- counters (work buffers H / yrows are allocated on the first layer call) ----
+  CK(cudaMalloc(&x->counters, sizeof(uint32_t) * 2 * x->nb1));
+  CK(cudaMemset(x->counters, 0, sizeof(uint32_t) * 2 * x->nb1));
+  CK(cudaMalloc(&x->routing, sizeof(int32_t) * (size_t)c.m_cap * c.topk));
+  ix.zero_words = x->counters;
+  ix.n_zero_words = 2 * x->nb1;
+
+  if (W == 1) {
+    comet_ctx* self = x;
+    if (int r2 = comet_link_local(&self, 1)) { comet_ctx_destroy(x); return r2; }
+  }
+  *out = x;
+  return COMET_OK;
+}
+
+int comet_ctx_destroy(comet_ctx* x) {
+  if (!x) return COMET_OK;
+  cudaSetDevice(x->cfg.device);
+  for (void* p : x->opened)
+    if (p) cudaIpcCloseMemHandle(p);
+  cudaFree(x->index_mem);
+  cudaFree(x->tiles_mem);
+  cudaFree(x->symm);
+  cudaFree(x->peer_tab);
+  cudaFree(x->H);
+  cudaFree(x->yrows);
+  cudaFree(x->counters);
+  cudaFree(x->routing);
+  delete x;
+  return COMET_OK;
+}
+
+static int upload_peer_table(comet_ctx* x, const std::vector<char*>& bases) {
+  const int W = x->cfg.world;
+  std::vector<void*> tab(4 * W);
+  const size_t off_tr = reinterpret_cast<char*>(x->tok_ready) - static_cast<char*>(x->symm);
+  (void)off_tr;
+  const size_t off_xr = reinterpret_cast<char*>(x->x_ready) - static_cast<char*>(x->symm);
+  const size_t off_cb = reinterpret_cast<char*>(x->cb) - static_cast<char*>(x->symm);
+  const size_t off_cf = reinterpret_cast<char*>(x->cb_flag) - static_cast<char*>(x->symm);
+  for (int r = 0; r < W; ++r) {
+    tab[r] = bases[r];
+    tab[W + r] = bases[r] + off_cb;
+    tab[2 * W + r] = bases[r] + off_cf;
+    tab[3 * W + r] = bases[r] + off_xr;
+  }
+  CK(cudaSetDevice(x->cfg.device));
+  CK(cudaMemcpy(x->peer_tab, tab.data(), sizeof(void*) * 4 * W, cudaMemcpyHostToDevice));
+  return COMET_OK;
+}
+
+int comet_symm_export(comet_ctx* x, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  CK(cudaSetDevice(x->cfg.device));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, x->symm));
+  memcpy(handle64, &h, 64);
+  return COMET_OK;
+}
+
+int comet_symm_import(comet_ctx* x, const void* handles) {
+  const int W = x->cfg.world;
+  CK(cudaSetDevice(x->cfg.device));
+  std::vector<char*> bases(W);
+  for (int r = 0; r < W; ++r) {
+    if (r == x->cfg.rank) {
+      bases[r] = static_cast<char*>(x->symm);
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + 64 * r, 64);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    x->opened[r] = p;
+    bases[r] = static_cast<char*>(p);
+  }
+  return upload_peer_table(x, bases);
+}
+
+int comet_link_local(comet_ctx** ctxs, int n) {
+  for (int i = 0; i < n; ++i) {
+    comet_ctx* x = ctxs[i];
+    if (x->cfg.world != n || x->cfg.rank != i)
+      return fail(COMET_EINVAL, "link_local: ctx %d has rank %d world %d", i, x->cfg.rank, x->cfg.world);
+    if (ctxs[0]->symm_bytes != x->symm_bytes) return fail(COMET_EINVAL, "link_local: asymmetric heaps");
+  }
+  std::vector<char*> bases(n);
+  for (int i = 0; i < n; ++i) bases[i] = static_cast<char*>(ctxs[i]->symm);
+  for (int i = 0; i < n; ++i) {
+    // peer access between devices when the group spans several GPUs
+    for (int j = 0; j < n; ++j) {
+      if (ctxs[j]->cfg.device != ctxs[i]->cfg.device) {
+        cudaSetDevice(ctxs[i]->cfg.device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[j]->cfg.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(COMET_ECUDA, "peer access %d->%d: %s", ctxs[i]->cfg.device, ctxs[j]->cfg.device,
+                      cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+    }
+    if (int rc = upload_peer_table(ctxs[i], bases)) return rc;
+  }
+  return COMET_OK;
+}
+
+void* comet_token_buffer(comet_ctx* x) { return x->xs; }
+void* comet_routing_buffer(comet_ctx* x) { return x->routing; }
+void* comet_hidden_buffer(comet_ctx* x) { return x->H; }
+void* comet_yrows_buffer(comet_ctx* x) { return x->yrows; }
+int32_t comet_hidden_rows_cap(comet_ctx* x) { return x->cap_rows_pad; }
+
+static int ensure_tiles(comet_ctx* x, int tile_rows, int tile_cols) {
+  const auto& c = x->cfg;
+  const long long t0 = (long long)x->cap_rows / tile_rows + x->E_r + 1;
+  const long long ch = (c.N + tile_cols - 1) / tile_cols;
+  const long long t1 = t0 * ch;
+  if (t0 <= x->cap_tiles0 && t1 <= x->cap_tiles1 && ch <= x->cap_chunks && x->tiles_mem) return COMET_OK;
+  if (t1 > (1ll << 28)) return fail(COMET_EINVAL, "tile list too large (tile_rows=%d tile_cols=%d)", tile_rows, tile_cols);
+  cudaFree(x->tiles_mem);
+  x->tiles_mem = nullptr;
+  const size_t n = align_up(t0 * 4, 64) + align_up(t1 * 6, 64) + align_up(ch * 4, 64);
+  CK(cudaMalloc(&x->tiles_mem, n * 4));
+  x->cap_tiles0 = (int)t0;
+  x->cap_tiles1 = (int)t1;
+  x->cap_chunks = (int)ch;
+  x->ix.tiles0 = x->tiles_mem;
+  x->ix.tiles1 = x->tiles_mem + align_up(t0 * 4, 64);
+  x->ix.chunks = x->ix.tiles1 + align_up(t1 * 6, 64);
+  x->ix.cap_tiles0 = (int)t0;
+  x->ix.cap_tiles1 = (int)t1;
+  return COMET_OK;
+}
+
+int comet_index_build(comet_ctx* x, const int32_t* d_experts, int M, int tile_rows, int tile_cols, void* stream) {
+  const auto& c = x->cfg;
+  if (M < 0 || M > c.m_cap) return fail(COMET_EINVAL, "M=%d outside [0, m_cap=%d]", M, c.m_cap);
+  if (tile_rows < 1) return fail(COMET_EINVAL, "tile_rows must be >= 1, got %d", tile_rows);
+  if (tile_cols < 1 || tile_cols > c.N) return fail(COMET_EINVAL, "tile_cols must be in [1, %d], got %d", c.N, tile_cols);
+  if (c.world * c.world > 4096) return fail(COMET_EINVAL, "world too large");
+  if (int rc = ensure_tiles(x, tile_rows, tile_cols)) return rc;
+  CK(cudaSetDevice(c.device));
+  x->M = M;
+  x->epoch += 1;
+  IndexDev ix = x->ix;
+  ix.experts = d_experts;
+  ix.M = M;
+  ix.E = c.E;
+  ix.topk = c.topk;
+  ix.tp = c.tp;
+  ix.ep = c.ep;
+  ix.rank = c.rank;
+  ix.world = c.world;
+  ix.e_lo = x->e_lo;
+  ix.E_r = x->E_r;
+  ix.tile_rows = tile_rows;
+  ix.tile_cols = tile_cols;
+  ix.n_embed = c.N;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(index_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIndexSmem));
+    attr_set = true;
+  }
+  index_build_kernel<<<x->E_r + 1, kIndexThreads, kIndexSmem, static_cast<cudaStream_t>(stream)>>>(ix);
+  CK(cudaGetLastError());
+  x->ix.experts = d_experts;  // the layer1 finish kernel reads the global routing
+  return COMET_OK;
+}
+
+int comet_index_sizes(comet_ctx* x, int32_t meta_out[16], void* stream) {
+  CK(cudaSetDevice(x->cfg.device));
+  CK(cudaMemcpyAsync(meta_out, x->ix.meta, 16 * 4, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  if (meta_out[kMetaSlots - 1]) return fail(COMET_ECAP, "index capacity exceeded (flags %d)", meta_out[kMetaSlots - 1]);
+  return COMET_OK;
+}
+
+int comet_index_download(comet_ctx* x, comet_index_host* h, void* stream) {
+  if (int rc = comet_index_sizes(x, h->meta, stream)) return rc;
+  const auto& c = x->cfg;
+  const int32_t* m = h->meta;
+  auto cp = [&](int32_t* dst, const int32_t* src, size_t n) -> int {
+    if (dst && n) CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyDeviceToHost));
+    return COMET_OK;
+  };
+  int rc = 0;
+  rc |= cp(h->counts, x->ix.counts, c.E);
+  rc |= cp(h->transfer, x->ix.transfer, (size_t)c.world * c.world);
+  rc |= cp(h->row_off, x->ix.row_off, x->E_r + 1);
+  rc |= cp(h->n_local, x->ix.n_local, x->E_r);
+  rc |= cp(h->row_token, x->ix.row_token, m[kMetaRows]);
+  rc |= cp(h->row_src, x->ix.row_src, m[kMetaRows]);
+  rc |= cp(h->tiles0, x->ix.tiles0, (size_t)m[kMetaTiles0] * 4);
+  rc |= cp(h->tiles1, x->ix.tiles1, (size_t)m[kMetaTiles1] * 6);
+  rc |= cp(h->chunks, x->ix.chunks, (size_t)m[kMetaChunks] * 4);
+  rc |= cp(h->pairs0, x->ix.pairs0, (size_t)m[kMetaPairs] * 4);
+  rc |= cp(h->pull_token, x->ix.pull_token, m[kMetaPull]);
+  rc |= cp(h->pull_src, x->ix.pull_src, m[kMetaPull]);
+  return rc ? COMET_ECUDA : COMET_OK;
+}
+
+int comet_signal_tokens_ready(comet_ctx* x, void* stream) {
+  CK(cudaSetDevice(x->cfg.device));
+  const int W = x->cfg.world;
+  signal_x_ready_kernel<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint32_t* const*>(x->peer_tab + 3 * W), x->cfg.rank, W, x->epoch);
+  CK(cudaGetLastError());
+  return COMET_OK;
+}
+
+// Layer work buffers + their TMA maps, allocated once on first use (an
+// index-only context -- resolver API -- never pays for them).
+static int ensure_work(comet_ctx* x) {
+  if (x->H) return COMET_OK;
+  const auto& c = x->cfg;
+  if (c.N % 64 || x->k_local % 64)
+    return fail(COMET_EINVAL, "N=%d and K/tp=%d must be multiples of 64 for the GPU layer (pad on the host)", c.N,
+                x->k_local);
+  CK(cudaSetDevice(c.device));
+  CK(cudaMalloc(&x->H, (size_t)x->cap_rows_pad * x->k_local * 2));
+  CK(cudaMalloc(&x->yrows, (size_t)x->cap_rows_pad * c.N * 2));
+  int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
+  if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
+  if (!rc) rc = make_map(&x->tm_y, x->yrows, x->cap_rows_pad, c.N, 128);
+  return rc;
+}
+
+static int get_weight_map(comet_ctx* x, MapCache& mc, const void* w, uint64_t rows, uint64_t cols) {
+  if (mc.ptr == w && mc.rows == rows && mc.cols == cols) return COMET_OK;
+  if (int rc = make_map(&mc.map, w, rows, cols, 128)) return rc;
+  mc.ptr = w;
+  mc.rows = rows;
+  mc.cols = cols;
+  return COMET_OK;
+}
+
+static LayerArgs base_args(comet_ctx* x) {
+  const auto& c = x->cfg;
+  LayerArgs a{};
+  a.rank = c.rank;
+  a.world = c.world;
+  a.tp = c.tp;
+  a.ep = c.ep;
+  a.M = x->M;
+  a.topk = c.topk;
+  a.n_embed = c.N;
+  a.k_local = x->k_local;
+  a.e_lo = x->e_lo;
+  a.experts_per_group = x->E_r;
+  a.epoch = x->epoch;
+  a.meta = x->ix.meta;
+  a.gather_row = x->ix.gather_row;
+  a.pull_token = x->ix.pull_token;
+  a.pull_src = x->ix.pull_src;
+  a.tok_pos = x->ix.tok_pos;
+  a.combine_tok = x->ix.combine_tok;
+  const int W = c.world;
+  a.xs_local = x->xs;
+  a.xs_peer = reinterpret_cast<const __nv_bfloat16* const*>(x->peer_tab);
+  a.cb_peer = reinterpret_cast<__nv_bfloat16* const*>(x->peer_tab + W);
+  a.cb_flag_peer = reinterpret_cast<uint32_t* const*>(x->peer_tab + 2 * W);
+  a.tok_ready = x->tok_ready;
+  a.x_ready = x->x_ready;
+  a.yrows = x->yrows;
+  a.nb_done = x->counters;
+  a.nb_sent = x->counters + x->nb1;
+  a.mloc_cap = x->mloc_cap;
+  return a;
+}
+
+static int launch_layer(comet_ctx* x, const LayerArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
+                        const CUtensorMap& to, int n_comm, cudaStream_t st) {
+  if (n_comm < 0 || (n_comm & 1)) return fail(COMET_EINVAL, "n_comm=%d must be even and >= 0", n_comm);
+  const int grid = std::min(x->n_sm, 2 * x->max_clusters);
+  LayerArgs b = a;
+  b.n_compute = grid - n_comm;
+  if (b.n_compute < 2) return fail(COMET_EINVAL, "n_comm=%d leaves no compute pair (grid %d)", n_comm, grid);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kLayerThreads);
+  lc.dynamicSmemBytes = kLayerSmem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, ta, tb, to, b));
+  return COMET_OK;
+}
+
+int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int group, void* stream) {
+  const auto& c = x->cfg;
+  if (activation < 0 || activation > COMET_ACT_TANH) return fail(COMET_EINVAL, "bad activation %d", activation);
+  if (group < 1) return fail(COMET_EINVAL, "group must be >= 1");
+  if (c.world == 1) n_comm = 0;
+  else if (n_comm < 2) return fail(COMET_EINVAL, "world > 1 needs n_comm >= 2 for layer0");
+  CK(cudaSetDevice(c.device));
+  if (int rc = ensure_work(x)) return rc;
+  if (int rc = get_weight_map(x, x->w0c, w0t, (uint64_t)x->E_r * x->k_local, c.N)) return rc;
+  LayerArgs a = base_args(x);
+  a.layer = 0;
+  a.n_blocks = x->nb0;
+  a.k_blocks = x->kb0;
+  a.b_rows = x->k_local;
+  a.order_group = group;
+  a.activation = activation;
+  a.pairs = x->ix.pairs0;
+  return launch_layer(x, a, x->tm_xs, x->w0c.map, x->tm_H, n_comm, static_cast<cudaStream_t>(stream));
+}
+
+int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_local, int n_comm, int wave,
+                 void* stream) {
+  const auto& c = x->cfg;
+  if (wave < 1) return fail(COMET_EINVAL, "wave must be >= 1");
+  if (n_comm < 2) return fail(COMET_EINVAL, "layer1 needs n_comm >= 2 (combine CTAs)");
+  CK(cudaSetDevice(c.device));
+  if (int rc = ensure_work(x)) return rc;
+  if (int rc = get_weight_map(x, x->w1c, w1t, (uint64_t)x->E_r * c.N, x->k_local)) return rc;
+  LayerArgs a = base_args(x);
+  a.layer = 1;
+  a.n_blocks = x->nb1;
+  a.k_blocks = x->kb1;
+  a.b_rows = c.N;
+  a.order_group = wave;
+  a.pairs = x->ix.pairs1;
+  a.combine_w = combine_w;
+  a.y_local = static_cast<__nv_bfloat16*>(y_local);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = launch_layer(x, a, x->tm_H, x->w1c.map, x->tm_y, n_comm, st)) return rc;
+  if (c.world > 1) {
+    combine_finish_kernel<<<x->n_sm, 256, 0, st>>>(a, x->cb, x->cb_flag, x->ix.experts);
+    CK(cudaGetLastError());
+  }
+  return COMET_OK;
+}
+
+int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t, const void* w1t,
+                  const float* combine_w, void* y_local, int activation, int n_comm0, int n_comm1, int group0,
+                  int wave1, void* stream) {
+  if (int rc = comet_index_build(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), stream))
+    return rc;
+  if (x->cfg.world > 1)
+    if (int rc = comet_signal_tokens_ready(x, stream)) return rc;
+  if (int rc = comet_layer0(x, w0t, activation, n_comm0, group0, stream)) return rc;
+  return comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// Parameters of the fused layer kernels (shared by host launcher and device).
+#pragma once
+
+#include <cstdint>
+
+#include "index.cuh"
+
+namespace comet {
+
+enum Activation : int { kActIdentity = 0, kActRelu = 1, kActSilu = 2, kActGeluTanh = 3, kActTanh = 4 };
+
+struct LayerArgs {
+  int layer;              // 0: dispatch + FC1 + act ; 1: FC2 + top-k combine
+  int rank, world, tp, ep;
+  int M, topk, n_embed;   // global tokens, experts per token, N
+  int k_local;            // K / tp
+  int e_lo;
+  int experts_per_group;  // E / ep
+  int n_compute;          // CTAs [0, n_compute) are compute (even); the rest comm
+  int n_blocks;           // output 256-col blocks of this layer
+  int k_blocks;           // 64-wide contraction blocks
+  int b_rows;             // weight rows per expert in the 2D B view
+  int order_group;        // layer0: pairs per group; layer1: n-blocks per wave
+  int activation;
+  uint32_t epoch;
+
+  // index (device)
+  const int32_t* meta;
+  const int32_t* pairs;       // [P*4] (e_local, pad_row, valid, key)
+  const int32_t* gather_row;  // [Rpad] token ids (layer0 A rows)
+  const int32_t* pull_token;  // layer0 comm
+  const int32_t* pull_src;
+  const int32_t* tok_pos;     // [M*topk]
+  const int32_t* combine_tok;
+  const float* combine_w;     // [M*topk] or null
+
+  // buffers
+  __nv_bfloat16* xs_local;        // [M_cap, N] this rank's symmetric token buffer
+  const __nv_bfloat16* const* xs_peer;  // [world] peer token buffers (device array)
+  uint32_t* tok_ready;            // [M_cap] epoch when xs_local[t] holds token t
+  const uint32_t* x_ready;        // [world] epoch when peer's own tokens are in place
+  const __nv_bfloat16* yrows;     // [Rpad_cap, N] layer1 per-(token,expert) rows
+  __nv_bfloat16* y_local;         // [M_r, N] final output (world == 1 or finish kernel)
+  __nv_bfloat16* const* cb_peer;  // [world] peer combine buffers [W*Mloc_cap, N]
+  uint32_t* const* cb_flag_peer;  // [world] peer flags [W * n_blocks]
+  uint32_t* nb_done;              // [n_blocks] layer1 compute completion counters
+  uint32_t* nb_sent;              // [n_blocks] layer1 comm CTA completion counters
+  int mloc_cap;                   // combine slots per sender
+
+  // per-CTA timeline (optional): [gridDim * cap] x (kind|task, start, end)
+  unsigned long long* timeline;
+  int timeline_cap;
+};
+
+}  // namespace comet
