@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -22,6 +23,10 @@ __global__ void moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const
 __global__ void combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb, const uint32_t* cb_flag,
                                       const int32_t* experts);
 __global__ void signal_x_ready_kernel(uint32_t* const* x_ready_peer, int rank, int world, uint32_t epoch);
+__global__ void dispatch_local_kernel(const int32_t* gather_row, const int32_t* meta, const __nv_bfloat16* xs,
+                                      __nv_bfloat16* xg, int n_embed, int M, int world, int rank);
+__global__ void combine_local_kernel(const int32_t* tok_pos, const float* combine_w, const __nv_bfloat16* yrows,
+                                     __nv_bfloat16* y, int t0, int n_tok, int topk, int n_embed);
 }  // namespace comet
 
 using namespace comet;
@@ -49,7 +54,7 @@ int fail(int code, const char* fmt, ...) {
 
 constexpr int kLayerThreads = 256;
 constexpr int kLayerStages = 6;
-constexpr size_t kLayerSmem = kLayerStages * 32768 + 2 * 16384 + 1024 + 256;
+constexpr size_t kLayerSmem = kLayerStages * 32768 + 2 * 16384 + 1024 + 1024;
 constexpr int kIndexThreads = 1024;
 constexpr size_t kIndexSmem = 8192 * sizeof(long long);
 
@@ -76,8 +81,10 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* e = getenv("COMET_L2PROMO")) promo = static_cast<CUtensorMapL2promotion>(atoi(e));
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(COMET_ECUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu", (int)r,
                                      (unsigned long long)rows, (unsigned long long)cols);
@@ -124,10 +131,12 @@ struct comet_ctx {
   // work buffers
   __nv_bfloat16* H = nullptr;
   __nv_bfloat16* yrows = nullptr;
+  __nv_bfloat16* xg = nullptr;      // dispatched (expert-sorted) layer0 rows
+  uint32_t* xg_ready = nullptr;     // per 128-row tile epoch
   uint32_t* counters = nullptr;  // nb_done[nb1] | nb_sent[nb1]
   int32_t* routing = nullptr;
 
-  CUtensorMap tm_xs, tm_H, tm_y;
+  CUtensorMap tm_xs, tm_H, tm_y, tm_xg;
   MapCache w0c, w1c;
 };
 
@@ -286,6 +295,8 @@ int comet_ctx_destroy(comet_ctx* x) {
   cudaFree(x->peer_tab);
   cudaFree(x->H);
   cudaFree(x->yrows);
+  cudaFree(x->xg);
+  cudaFree(x->xg_ready);
   cudaFree(x->counters);
   cudaFree(x->routing);
   delete x;
@@ -474,13 +485,19 @@ int comet_signal_tokens_ready(comet_ctx* x, void* stream) {
 static int ensure_work(comet_ctx* x) {
   if (x->H) return COMET_OK;
   const auto& c = x->cfg;
+  if (c.N * 2 > 20480) return fail(COMET_EINVAL, "N=%d too large for the dispatch ring (N <= 10240)", c.N);
+  if (c.topk > 8) return fail(COMET_EINVAL, "topk=%d > 8 unsupported by the combine engine", c.topk);
   if (c.N % 64 || x->k_local % 64)
     return fail(COMET_EINVAL, "N=%d and K/tp=%d must be multiples of 64 for the GPU layer (pad on the host)", c.N,
                 x->k_local);
   CK(cudaSetDevice(c.device));
   CK(cudaMalloc(&x->H, (size_t)x->cap_rows_pad * x->k_local * 2));
   CK(cudaMalloc(&x->yrows, (size_t)x->cap_rows_pad * c.N * 2));
+  CK(cudaMalloc(&x->xg, (size_t)x->cap_rows_pad * c.N * 2));
+  CK(cudaMalloc(&x->xg_ready, sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
+  CK(cudaMemset(x->xg_ready, 0, sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
   int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
+  if (!rc) rc = make_map(&x->tm_xg, x->xg, x->cap_rows_pad, c.N, 128);
   if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
   if (!rc) rc = make_map(&x->tm_y, x->yrows, x->cap_rows_pad, c.N, 128);
   return rc;
@@ -498,6 +515,7 @@ static int get_weight_map(comet_ctx* x, MapCache& mc, const void* w, uint64_t ro
 static LayerArgs base_args(comet_ctx* x) {
   const auto& c = x->cfg;
   LayerArgs a{};
+  if (const char* d = getenv("COMET_DEBUG")) a.debug = atoi(d);
   a.rank = c.rank;
   a.world = c.world;
   a.tp = c.tp;
@@ -511,6 +529,10 @@ static LayerArgs base_args(comet_ctx* x) {
   a.epoch = x->epoch;
   a.meta = x->ix.meta;
   a.gather_row = x->ix.gather_row;
+  a.pad_off = x->ix.pad_off;
+  a.n_local = x->ix.n_local;
+  a.xg = x->xg;
+  a.xg_ready = x->xg_ready;
   a.pull_token = x->ix.pull_token;
   a.pull_src = x->ix.pull_src;
   a.tok_pos = x->ix.tok_pos;
@@ -532,7 +554,8 @@ static LayerArgs base_args(comet_ctx* x) {
 static int launch_layer(comet_ctx* x, const LayerArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& to, int n_comm, cudaStream_t st) {
   if (n_comm < 0 || (n_comm & 1)) return fail(COMET_EINVAL, "n_comm=%d must be even and >= 0", n_comm);
-  const int grid = std::min(x->n_sm, 2 * x->max_clusters);
+  int grid = std::min(x->n_sm, 2 * x->max_clusters);
+  if (const char* e = getenv("COMET_GRID")) grid = std::min(grid, atoi(e));
   LayerArgs b = a;
   b.n_compute = grid - n_comm;
   if (b.n_compute < 2) return fail(COMET_EINVAL, "n_comm=%d leaves no compute pair (grid %d)", n_comm, grid);
@@ -556,8 +579,8 @@ int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int 
   const auto& c = x->cfg;
   if (activation < 0 || activation > COMET_ACT_TANH) return fail(COMET_EINVAL, "bad activation %d", activation);
   if (group < 1) return fail(COMET_EINVAL, "group must be >= 1");
-  if (c.world == 1) n_comm = 0;
-  else if (n_comm < 2) return fail(COMET_EINVAL, "world > 1 needs n_comm >= 2 for layer0");
+  if (c.world > 1 && n_comm < 2) return fail(COMET_EINVAL, "world > 1: layer0 needs n_comm >= 2 (NVLink dispatch CTAs)");
+  if (c.world == 1) n_comm = 0;  // no remote rows: every row is placed by the local dispatch
   CK(cudaSetDevice(c.device));
   if (int rc = ensure_work(x)) return rc;
   if (int rc = get_weight_map(x, x->w0c, w0t, (uint64_t)x->E_r * x->k_local, c.N)) return rc;
@@ -569,14 +592,19 @@ int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int 
   a.order_group = group;
   a.activation = activation;
   a.pairs = x->ix.pairs0;
-  return launch_layer(x, a, x->tm_xs, x->w0c.map, x->tm_H, n_comm, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // HBM-local rows first (whole GPU, bandwidth-bound); comm CTAs pull only remote rows.
+  dispatch_local_kernel<<<x->n_sm * 4, 256, 0, st>>>(x->ix.gather_row, x->ix.meta, x->xs, x->xg, c.N, x->M, c.world,
+                                                     c.rank);
+  CK(cudaGetLastError());
+  return launch_layer(x, a, x->tm_xg, x->w0c.map, x->tm_H, n_comm, st);
 }
 
 int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_local, int n_comm, int wave,
                  void* stream) {
   const auto& c = x->cfg;
   if (wave < 1) return fail(COMET_EINVAL, "wave must be >= 1");
-  if (n_comm < 2) return fail(COMET_EINVAL, "layer1 needs n_comm >= 2 (combine CTAs)");
+  if (c.world > 1 && n_comm < 2) return fail(COMET_EINVAL, "world > 1: layer1 needs n_comm >= 2 (combine CTAs)");
   CK(cudaSetDevice(c.device));
   if (int rc = ensure_work(x)) return rc;
   if (int rc = get_weight_map(x, x->w1c, w1t, (uint64_t)x->E_r * c.N, x->k_local)) return rc;
@@ -591,7 +619,13 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   a.y_local = static_cast<__nv_bfloat16*>(y_local);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (int rc = launch_layer(x, a, x->tm_H, x->w1c.map, x->tm_y, n_comm, st)) return rc;
-  if (c.world > 1) {
+  if (n_comm == 0) {
+    const int t0 = token_start_of(c.rank, x->M, c.world);
+    const int n_tok = token_stop_of(c.rank, x->M, c.world) - t0;
+    combine_local_kernel<<<x->n_sm * 8, 256, 0, st>>>(x->ix.tok_pos, combine_w, x->yrows,
+                                                      static_cast<__nv_bfloat16*>(y_local), t0, n_tok, c.topk, c.N);
+    CK(cudaGetLastError());
+  } else if (c.world > 1) {
     combine_finish_kernel<<<x->n_sm, 256, 0, st>>>(a, x->cb, x->cb_flag, x->ix.experts);
     CK(cudaGetLastError());
   }

@@ -1,0 +1,273 @@
+// Communication-CTA roles of the fused layer kernels (section 3.2.1,
+// thread-block specialisation).  A communication CTA is a TMA bulk-copy
+// engine: a loader warp computes the descriptors of kBatch jobs at a time
+// (lane-parallel index loads), then each lane streams its job's row segments
+// -- from local HBM or NVLink-mapped peer memory -- into its own smem ring
+// slot; consumer warps drain the slots (bulk-store them, or reduce them).
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "layers.cuh"
+#include "ptx.cuh"
+
+namespace comet {
+namespace comm {
+
+constexpr int kMaxSlots = 224;
+constexpr int kReducers = 7;               // combine: warps 1..7
+constexpr int kBatch = 16;                 // jobs described per loader pass
+constexpr uint32_t kRingBytes = 160 * 1024;
+constexpr int kFreeLag = 8;                // dispatch: bulk-store groups before a slot is reused
+constexpr int kPubLag = 24;                // dispatch: groups in flight before a tile is published
+
+struct JobDesc {
+  __nv_bfloat16* dst;
+  float w[8];
+};
+
+struct CommSmem {
+  uint64_t full[kMaxSlots];
+  uint64_t empty[kMaxSlots];
+  JobDesc desc[kMaxSlots];
+  int pub_tile[64];
+  int pub_job[64];
+  const __nv_bfloat16* xs_peer[kMaxWorld];
+};
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ CommSmem* comm_smem(uint8_t* smem) {
+  return reinterpret_cast<CommSmem*>(smem + kRingBytes);
+}
+
+__device__ __forceinline__ void comm_init(const LayerArgs& p, uint8_t* smem, int n_slots) {
+  CommSmem* cs = comm_smem(smem);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n_slots; ++i) {
+      ptx::mbar_init(cs->full + i, 1);
+      ptx::mbar_init(cs->empty + i, 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (static_cast<int>(threadIdx.x) < p.world) cs->xs_peer[threadIdx.x] = p.xs_peer[threadIdx.x];
+  __syncthreads();
+}
+
+// Remote (NVLink) rows of 128-row tile q of the claim-ordered pair table: the
+// local rows of every expert block are a prefix (resolver.py:171-195) and were
+// already placed by dispatch_local_kernel, so a tile's remote rows are the
+// suffix [padrow0, padrow0 + nr).  Returns false for tiles without any.
+__device__ __forceinline__ bool remote_rows(const LayerArgs& p, int q, int& padrow0, int& nr) {
+  const int4 pr = reinterpret_cast<const int4*>(p.pairs)[q >> 1];
+  if (!((pr.w >> (q & 1)) & 1)) return false;
+  const int base = pr.y + kTileRows * (q & 1);
+  const int rows = max(0, min(kTileRows, pr.z - kTileRows * (q & 1)));
+  const int rel = base - p.pad_off[pr.x];                        // tile start within the expert block
+  const int first = min(rows, max(0, p.n_local[pr.x] - rel));      // first remote row of the tile
+  padrow0 = base + first;
+  nr = rows - first;
+  return nr > 0;
+}
+
+// layer0 dispatch: fill the expert-sorted shared tensor xg tile by tile in the
+// compute schedule's claim order (locality-first, resolver.py:206-252): local
+// rows from this rank's token buffer, remote rows pulled over NVLink from the
+// source rank's token buffer; publish each 128-row tile with a ready epoch.
+__device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
+  const uint32_t row_bytes = static_cast<uint32_t>(p.n_embed) * 2u;  // <= kRingBytes / 8 (host-checked)
+  const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / row_bytes));
+  comm_init(p, smem, n_slots);
+  CommSmem* cs = comm_smem(smem);
+  const int n_comm = gridDim.x - p.n_compute;
+  const int cid = blockIdx.x - p.n_compute;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = p.meta[kMetaPairs];
+  const int n_tiles = 2 * P;
+  if (warp == 0) {
+    // ---- loader warp ----
+    uint64_t ready_mask = 1ull << p.rank;
+    int k = 0;
+    for (int q = cid; q < n_tiles; q += n_comm) {
+      int padrow0, nr;
+      if (!remote_rows(p, q, padrow0, nr)) continue;
+      for (int r0 = 0; r0 < nr; r0 += kBatch) {
+        const int r = r0 + lane;
+        if (lane < kBatch && r < nr) {
+          const int t = p.gather_row[padrow0 + r];
+          const int src = src_rank_of(t, p.M, p.world);
+          if (!((ready_mask >> src) & 1)) {
+            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + src), p.epoch)) __nanosleep(64);
+            ready_mask |= 1ull << src;
+          }
+          const int job = k + lane;
+          const int slot = job % n_slots;
+          ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(cs->full + slot, row_bytes);
+          ptx::bulk_load(smem + slot * row_bytes, cs->xs_peer[src] + static_cast<long long>(t) * p.n_embed,
+                         row_bytes, cs->full + slot);
+        }
+        k += min(kBatch, nr - r0);
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- storer: slot -> xg row; publish tiles once their writes landed ----
+    int k = 0, head = 0, tail = 0;
+    auto publish_upto = [&](int done_job) {
+      while (head != tail && cs->pub_job[head & 63] <= done_job) {
+        ptx::fence_async_global();
+        ptx::st_release_gpu(p.xg_ready + cs->pub_tile[head & 63], p.epoch);
+        ++head;
+      }
+    };
+    for (int q = cid; q < n_tiles; q += n_comm) {
+      int padrow0, nr;
+      if (!remote_rows(p, q, padrow0, nr)) continue;
+      for (int r = 0; r < nr; ++r, ++k) {
+        const int slot = k % n_slots;
+        ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
+        ptx::bulk_store(p.xg + static_cast<long long>(padrow0 + r) * p.n_embed, smem + slot * row_bytes, row_bytes);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read<kFreeLag>();
+        if (k >= kFreeLag) ptx::mbar_arrive(cs->empty + (k - kFreeLag) % n_slots);
+        if (k >= kPubLag) {
+          ptx::bulk_wait<kPubLag>();
+          publish_upto(k - kPubLag);
+        }
+      }
+      cs->pub_tile[tail & 63] = q;
+      cs->pub_job[tail & 63] = k - 1;
+      ++tail;
+      if (tail - head >= 60) {
+        ptx::bulk_wait<0>();
+        publish_upto(k);
+      }
+    }
+    ptx::bulk_wait<0>();
+    publish_upto(k);
+  }
+}
+
+// layer1 combine: once every pair finished column block nb, reduce each
+// hosted token's expert rows (ascending slot = ascending expert, weighted when
+// combine weights are given; executor.py:102-120) and write the result to the
+// output (world == 1) or push the partial row to the token's source rank.
+__device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
+  const int K = p.topk, N = p.n_embed, NB = p.n_blocks;
+  constexpr uint32_t kSeg = kBlockN * 2;  // 512 B of one expert row per column block
+  const uint32_t slot_bytes = K * kSeg;
+  const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / slot_bytes)) / kReducers * kReducers;
+  comm_init(p, smem, n_slots);
+  CommSmem* cs = comm_smem(smem);
+  const int n_comm = gridDim.x - p.n_compute;
+  const int cid = blockIdx.x - p.n_compute;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = p.meta[kMetaPairs];
+  const int n_tok = p.meta[kMetaCombineTok];
+  const uint32_t target = 2u * static_cast<uint32_t>(P);
+  const int start_r = token_start_of(p.rank, p.M, p.world);
+  const int jobs = n_tok > cid ? (n_tok - cid + n_comm - 1) / n_comm : 0;  // tokens of this CTA per nb
+  if (warp == 0) {
+    // ---- loader warp ----
+    if (p.world > 1) {  // every peer finished its previous forward (epoch barrier)
+      if (lane < p.world)
+        while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + lane), p.epoch)) __nanosleep(64);
+      __syncwarp();
+    }
+    int k = 0;
+    for (int nb = 0; nb < NB; ++nb) {
+      if (lane == 0)
+        while (ptx::ld_acquire_gpu(p.nb_done + nb) < target) __nanosleep(128);
+      __syncwarp();
+      const uint32_t seg = min(kSeg, static_cast<uint32_t>(N - nb * kBlockN) * 2u);
+      for (int j0 = 0; j0 < jobs; j0 += kBatch) {
+        const int j = j0 + lane;
+        if (lane < kBatch && j < jobs) {
+          const int t = p.combine_tok[cid + j * n_comm];
+          const int job = k + lane;
+          const int slot = job % n_slots;
+          JobDesc d;
+          uint32_t bytes = 0;
+          int pos[8];
+          for (int s = 0; s < K; ++s) {
+            pos[s] = p.tok_pos[t * K + s];
+            d.w[s] = pos[s] < 0 ? 0.f : (p.combine_w ? p.combine_w[t * K + s] : 1.f);
+            bytes += pos[s] >= 0 ? seg : 0u;
+          }
+          if (p.world == 1) {
+            d.dst = p.y_local + static_cast<long long>(t - start_r) * N + nb * kBlockN;
+          } else {
+            const int dr = src_rank_of(t, p.M, p.world);
+            const int cslot = p.rank * p.mloc_cap + (t - token_start_of(dr, p.M, p.world));
+            d.dst = p.cb_peer[dr] + static_cast<long long>(cslot) * N + nb * kBlockN;
+          }
+          ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
+          cs->desc[slot] = d;
+          ptx::mbar_arrive_expect_tx(cs->full + slot, bytes);  // release: desc visible to the reducer
+          for (int s = 0; s < K; ++s)
+            if (pos[s] >= 0)
+              ptx::bulk_load(smem + slot * slot_bytes + s * kSeg,
+                             p.yrows + static_cast<long long>(pos[s]) * N + nb * kBlockN, seg, cs->full + slot);
+        }
+        k += min(kBatch, jobs - j0);
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  // ---- reducers: warp w takes jobs k with k % kReducers == w - 1 ----
+  const int me = warp - 1;
+  int k = 0;
+  for (int nb = 0; nb < NB; ++nb) {
+    const bool col_ok = nb * kBlockN + lane * 8 < N;
+    for (int j = 0; j < jobs; ++j, ++k) {
+      if (k % kReducers != me) continue;
+      const int slot = k % n_slots;
+      ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
+      const JobDesc& d = cs->desc[slot];
+      float acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+      for (int s = 0; s < K; ++s) {
+        const float w = d.w[s];
+        if (w == 0.f) continue;
+        const uint4 v = *reinterpret_cast<const uint4*>(smem + slot * slot_bytes + s * kSeg + lane * 16);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float2 f = __bfloat1622float2(h[c]);
+          acc[2 * c] += f.x * w;
+          acc[2 * c + 1] += f.y * w;
+        }
+      }
+      __nv_bfloat16* dst = d.dst + lane * 8;
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(cs->empty + slot);
+      if (col_ok) {
+        uint4 o;
+        o.x = pack2(acc[0], acc[1]); o.y = pack2(acc[2], acc[3]);
+        o.z = pack2(acc[4], acc[5]); o.w = pack2(acc[6], acc[7]);
+        ptx::st_v4(dst, o);
+      }
+    }
+    if (p.world > 1) {
+      // all reducers of this CTA finished nb -> count the CTA; last CTA signals peers
+      __threadfence_system();
+      ptx::named_bar_sync(2, kReducers * 32);
+      if (threadIdx.x == 32) {
+        const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.nb_sent + nb, 1u);
+        if (prev == static_cast<uint32_t>(n_comm) - 1) {
+          ptx::fence_acq_rel_sys();
+          for (int d = 0; d < p.world; ++d) ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * NB + nb, p.epoch);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace comm
+}  // namespace comet

@@ -312,8 +312,13 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
         rank += kq < key;
       }
       ix.pair_key[i] = rank;
+      // .w: bit h set when 128-row half h holds rows pulled from other ranks
+      const int r0 = prow - s_pad[j];
+      const int remote_mask = (min(r0 + kTileRows, s_cnt[ix.e_lo + j]) > s_nloc[j] ? 1 : 0) |
+                              (valid > kTileRows && r0 + valid > s_nloc[j] ? 2 : 0);
       int* o0 = ix.pairs0 + rank * 4;
-      o0[0] = j; o0[1] = prow; o0[2] = valid; o0[3] = i;
+      o0[0] = j; o0[1] = prow; o0[2] = valid; o0[3] = remote_mask;
+      o[3] = remote_mask;
     }
   }
   __syncthreads();

@@ -23,11 +23,16 @@ struct LayerArgs {
   int order_group;        // layer0: pairs per group; layer1: n-blocks per wave
   int activation;
   uint32_t epoch;
+  int debug;              // bit0: comm CTAs idle; bit1: layer0 A by 2D tile (no gather); bit2: spin waits
 
   // index (device)
   const int32_t* meta;
   const int32_t* pairs;       // [P*4] (e_local, pad_row, valid, key)
-  const int32_t* gather_row;  // [Rpad] token ids (layer0 A rows)
+  const int32_t* gather_row;  // [Rpad] token ids of the padded layout (-1 = padding)
+  const int32_t* pad_off;     // [E_r+1] padded block offset of each hosted expert
+  const int32_t* n_local;     // [E_r] local (prefix) rows of each hosted expert
+  __nv_bfloat16* xg;          // [Rpad_cap, N] layer0 A: dispatched rows, expert-sorted
+  uint32_t* xg_ready;         // [Rpad_cap / 128] epoch when a 128-row tile of xg is filled
   const int32_t* pull_token;  // layer0 comm
   const int32_t* pull_src;
   const int32_t* tok_pos;     // [M*topk]

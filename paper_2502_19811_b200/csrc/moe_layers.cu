@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "comm.cuh"
 #include "layers.cuh"
 #include "ptx.cuh"
 
@@ -41,7 +42,6 @@ constexpr uint32_t kAccCols = kBlockN;                  // fp32 columns per accu
 constexpr uint32_t kTmemCols = 2 * kAccCols;
 constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(2 * kTileRows, kBlockN);
 constexpr int kEpiThread0 = 128;                        // first epilogue thread
-constexpr int kCommWarps = kThreads / 32;
 
 struct Unit {
   int pair, nb;
@@ -91,121 +91,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// ------------------------------------------------------------ comm roles --
-// layer0: pull distinct remote tokens (first-demand order) into xs_local.
-__device__ void dispatch_pull(const LayerArgs& p) {
-  const int n_comm = gridDim.x - p.n_compute;
-  const int cid = blockIdx.x - p.n_compute;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_pull = p.meta[kMetaPull];
-  const int row_vec = p.n_embed / 8;  // uint4 per row
-  uint64_t ready_mask = 0;            // peers whose tokens are known in place
-  for (int q = cid * kCommWarps + warp; q < n_pull; q += n_comm * kCommWarps) {
-    const int t = p.pull_token[q], src = p.pull_src[q];
-    if (!((ready_mask >> src) & 1)) {
-      if (lane == 0)
-        while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + src), p.epoch)) __nanosleep(64);
-      __syncwarp();
-      ready_mask |= 1ull << src;
-    }
-    const uint4* s = reinterpret_cast<const uint4*>(p.xs_peer[src] + static_cast<long long>(t) * p.n_embed);
-    uint4* d = reinterpret_cast<uint4*>(p.xs_local + static_cast<long long>(t) * p.n_embed);
-    int i = lane;
-    for (; i + 96 < row_vec; i += 128) {
-      const uint4 a = ptx::ld_nc_v4(s + i), b = ptx::ld_nc_v4(s + i + 32);
-      const uint4 c = ptx::ld_nc_v4(s + i + 64), e = ptx::ld_nc_v4(s + i + 96);
-      ptx::st_v4(d + i, a); ptx::st_v4(d + i + 32, b);
-      ptx::st_v4(d + i + 64, c); ptx::st_v4(d + i + 96, e);
-    }
-    for (; i < row_vec; i += 32) ptx::st_v4(d + i, ptx::ld_nc_v4(s + i));
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) ptx::st_release_gpu(p.tok_ready + t, p.epoch);
-  }
-}
-
-// layer1: per finished n-block, top-k reduce of each hosted token.
-__device__ void combine_reduce(const LayerArgs& p) {
-  const int n_comm = gridDim.x - p.n_compute;
-  const int cid = blockIdx.x - p.n_compute;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int P = p.meta[kMetaPairs];
-  const int n_tok = p.meta[kMetaCombineTok];
-  const int NB = p.n_blocks, K = p.topk, N = p.n_embed;
-  const uint32_t target = 2u * static_cast<uint32_t>(P);
-  const int start_r = token_start_of(p.rank, p.M, p.world);
-  if (p.world > 1) {
-    // Every peer has finished its previous forward (it signalled this epoch's
-    // tokens), so its combine buffer and flags may be overwritten.
-    if (threadIdx.x < p.world)
-      while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + threadIdx.x), p.epoch)) __nanosleep(64);
-    __syncthreads();
-  }
-  for (int nb = 0; nb < NB; ++nb) {
-    if (threadIdx.x == 0) {
-      while (ptx::ld_acquire_gpu(p.nb_done + nb) < target) __nanosleep(128);
-    }
-    __syncthreads();
-    const int col = nb * kBlockN + lane * 8;
-    const bool col_ok = col < N;
-    for (int i = cid * kCommWarps + warp; col_ok && i < n_tok; i += n_comm * kCommWarps) {
-      const int t = p.combine_tok[i];
-      float acc[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = 0.f;
-      for (int s = 0; s < K; ++s) {
-        const int pos = p.tok_pos[t * K + s];
-        if (pos < 0) continue;
-        const float w = p.combine_w ? p.combine_w[t * K + s] : 1.f;
-        const uint4 v = ptx::ld_v4(p.yrows + static_cast<long long>(pos) * N + col);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float2 f = __bfloat1622float2(h[c]);
-          acc[2 * c] += (p.combine_w ? f.x * w : f.x);
-          acc[2 * c + 1] += (p.combine_w ? f.y * w : f.y);
-        }
-      }
-      uint4 o;
-      o.x = pack_bf16(acc[0], acc[1]); o.y = pack_bf16(acc[2], acc[3]);
-      o.z = pack_bf16(acc[4], acc[5]); o.w = pack_bf16(acc[6], acc[7]);
-      if (p.world == 1) {
-        ptx::st_v4(p.y_local + static_cast<long long>(t - start_r) * N + col, o);
-      } else {
-        const int dst = src_rank_of(t, p.M, p.world);
-        const int slot = p.rank * p.mloc_cap + (t - token_start_of(dst, p.M, p.world));
-        ptx::st_v4(p.cb_peer[dst] + static_cast<long long>(slot) * N + col, o);
-      }
-    }
-    if (p.world > 1) {
-      __threadfence_system();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.nb_sent + nb, 1u);
-        if (prev == static_cast<uint32_t>(n_comm) - 1) {
-          ptx::fence_acq_rel_sys();
-          for (int d = 0; d < p.world; ++d)
-            ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * NB + nb, p.epoch);
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1)
 moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                  const __grid_constant__ CUtensorMap tm_out, const LayerArgs p) {
-  if (static_cast<int>(blockIdx.x) >= p.n_compute) {
-    if (p.layer == 0) dispatch_pull(p);
-    else combine_reduce(p);
-    return;
-  }
-
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (static_cast<int>(blockIdx.x) >= p.n_compute) {
+    if (p.debug & 1) return;
+    if (p.layer == 0) comm::dispatch_rows(p, smem);
+    else comm::combine_reduce(p, smem);
+    return;
+  }
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kSmemStage + 2 * kSmemEpi);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
@@ -215,6 +113,11 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = blockIdx.x & 1;  // rank in the 2-CTA cluster
+  const bool spin = (p.debug & 4) != 0;
+  auto wait = [spin](uint64_t* bar, uint32_t parity) {
+    if (spin) ptx::mbar_wait_spin(bar, parity);
+    else ptx::mbar_wait(bar, parity);
+  };
   const bool leader = cta == 0;
 
   if (warp == 0 && lane == 0) {
@@ -254,31 +157,23 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta);
-      int4 tok = make_int4(-1, -1, -1, -1);
-      if (p.layer == 0) {
-        tok = reinterpret_cast<const int4*>(p.gather_row + row0)[lane];
-        if (p.world > 1) {
-          const int tt[4] = {tok.x, tok.y, tok.z, tok.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int t = tt[i];
-            if (t >= 0 && src_rank_of(t, p.M, p.world) != p.rank)
-              while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.tok_ready + t), p.epoch)) __nanosleep(32);
-          }
-          ptx::fence_async_global();
-          __syncwarp();
-        }
+      if (p.layer == 0 && ((pr.w >> cta) & 1) && !(p.debug & 1) && lane == 0) {
+        // this CTA's 128 A rows include rows pulled over NVLink by a comm CTA
+        const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
+        while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) __nanosleep(32);
+        ptx::fence_async_global();
       }
+      __syncwarp();
       for (int kb = 0; kb < p.k_blocks; ++kb) {
-        ptx::mbar_wait(empty + stage, phase ^ 1);
-        uint8_t* sa = smem + stage * kSmemStage;
-        uint8_t* sb = sa + kSmemA;
-        if (p.layer == 0) {
-          ptx::tma_gather4_2sm(sa + lane * 512, &tm_a, full + stage, kb * kBlockK, tok.x, tok.y, tok.z, tok.w);
+        wait(empty + stage, phase ^ 1);
+        if (lane == 0 && (p.debug & 16)) {
+          // debug: no data movement, complete the stage by arrivals only
+          if (leader) ptx::mbar_arrive(full + stage);
+          else ptx::mbar_arrive_cluster(full + stage, 0);
         } else if (lane == 0) {
+          uint8_t* sa = smem + stage * kSmemStage;
+          uint8_t* sb = sa + kSmemA;
           ptx::tma_load_2d_2sm(sa, &tm_a, full + stage, kb * kBlockK, row0, ptx::kEvictNormal);
-        }
-        if (lane == 0) {
           ptx::tma_load_2d_2sm(sb, &tm_b, full + stage, kb * kBlockK, brow, ptx::kEvictNormal);
           if (leader) ptx::mbar_arrive_expect_tx(full + stage, 2 * kSmemStage);
           else ptx::mbar_arrive_cluster(full + stage, 0);
@@ -295,19 +190,21 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
       const int a = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      ptx::mbar_wait(tempty + a, aphase ^ 1);
+      wait(tempty + a, aphase ^ 1);
       ptx::tc_fence_after();
       const uint32_t dcol = tmem_base + a * kAccCols;
       for (int kb = 0; kb < p.k_blocks; ++kb) {
-        ptx::mbar_wait(full + stage, phase);
+        wait(full + stage, phase);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           const uint32_t sa = ptx::smem_u32(smem + stage * kSmemStage);
+          if (!(p.debug & 8)) {
           const uint64_t da = ptx::sdesc_kmajor_sw128(sa);
           const uint64_t db = ptx::sdesc_kmajor_sw128(sa + kSmemA);
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
             ptx::mma_bf16_2sm(dcol, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
+          }
           ptx::mma_commit_2sm(empty + stage, 0x3);
           if (kb == p.k_blocks - 1) ptx::mma_commit_2sm(tfull + a, 0x3);
         }
@@ -326,7 +223,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       const int a = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      ptx::mbar_wait(tfull + a, aphase);
+      wait(tfull + a, aphase);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + a * kAccCols;
 #pragma unroll 1
@@ -421,6 +318,71 @@ __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, 
     o.x = pack_bf16(acc[0], acc[1]); o.y = pack_bf16(acc[2], acc[3]);
     o.z = pack_bf16(acc[4], acc[5]); o.w = pack_bf16(acc[6], acc[7]);
     ptx::st_v4(p.y_local + static_cast<long long>(lt) * N + c, o);
+  }
+}
+
+// Local half of the layer0 dispatch: copy every row whose token lives on this
+// rank from the token buffer into its slot of the expert-sorted shared tensor
+// (HBM-bound; one warp per row, 16 B per lane per access, whole GPU).
+__global__ void __launch_bounds__(256) dispatch_local_kernel(const int32_t* __restrict__ gather_row,
+                                                             const int32_t* __restrict__ meta,
+                                                             const __nv_bfloat16* __restrict__ xs,
+                                                             __nv_bfloat16* __restrict__ xg, int n_embed, int M,
+                                                             int world, int rank) {
+  const int rows = meta[kMetaRowsPad];
+  const int vec = n_embed / 8;
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const int t = gather_row[r];
+    if (t < 0 || src_rank_of(t, M, world) != rank) continue;
+    const uint4* s = reinterpret_cast<const uint4*>(xs + static_cast<long long>(t) * n_embed);
+    uint4* d = reinterpret_cast<uint4*>(xg + static_cast<long long>(r) * n_embed);
+    int i = lane;
+    for (; i + 7 * 32 < vec; i += 8 * 32) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ptx::ld_nc_v4(s + i + u * 32);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[i + u * 32] = v[u];
+    }
+    for (; i < vec; i += 32) d[i] = ptx::ld_nc_v4(s + i);
+  }
+}
+
+// Local top-k combine after layer1 (world == 1, or n_comm == 0): y[t] = left
+// fold over t's expert rows in ascending slot order, weighted when combine
+// weights are given (executor.py:102-120).  HBM-bound, whole GPU.
+__global__ void __launch_bounds__(256) combine_local_kernel(const int32_t* __restrict__ tok_pos,
+                                                            const float* __restrict__ combine_w,
+                                                            const __nv_bfloat16* __restrict__ yrows,
+                                                            __nv_bfloat16* __restrict__ y, int t0, int n_tok,
+                                                            int topk, int n_embed) {
+  const int vec = n_embed / 8;
+  const long long items = static_cast<long long>(n_tok) * vec;
+  for (long long it = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; it < items;
+       it += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int lt = static_cast<int>(it / vec), c = static_cast<int>(it % vec) * 8;
+    const int t = t0 + lt;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int s = 0; s < topk; ++s) {
+      const int pos = tok_pos[t * topk + s];
+      if (pos < 0) continue;
+      const float w = combine_w ? combine_w[t * topk + s] : 1.f;
+      const uint4 v = ptx::ld_nc_v4(yrows + static_cast<long long>(pos) * n_embed + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        acc[2 * j] += f.x * w;
+        acc[2 * j + 1] += f.y * w;
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16(acc[0], acc[1]); o.y = pack_bf16(acc[2], acc[3]);
+    o.z = pack_bf16(acc[4], acc[5]); o.w = pack_bf16(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(y + static_cast<long long>(lt) * n_embed + c) = o;
   }
 }
 

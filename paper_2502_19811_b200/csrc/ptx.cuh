@@ -76,6 +76,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       :: "r"(addr), "r"(parity) : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITS_%=;\n\t}"
+      :: "r"(addr), "r"(parity) : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
@@ -89,7 +99,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
+  // Plain (default-semantics) remote arrive.  A `.release.cluster` arrive
+  // waits for this thread's in-flight TMA loads and serialises the pipeline
+  // (measured 4x lower per-SM load rate, tools/tma_bench.cu modes 2 vs 3).
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
 }
 
 // ------------------------------------------------------------------ TMA --
@@ -120,6 +133,16 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const void* tmap, uin
          "r"(c0), "r"(c1), "l"(hint) : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_2sm_nohint(void* dst, const void* tmap, uint64_t* bar,
+                                                       int32_t c0, int32_t c1) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader),
+         "r"(c0), "r"(c1) : "memory");
+}
+
 // Row gather: four rows (r0..r3) x box-width columns starting at column c0.
 // cta_group::2 lets the completion go to the leader CTA's barrier.
 __device__ __forceinline__ void tma_gather4_2sm(void* dst, const void* tmap, uint64_t* bar,
@@ -131,6 +154,17 @@ __device__ __forceinline__ void tma_gather4_2sm(void* dst, const void* tmap, uin
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
       :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader),
          "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+}
+
+// 1-D bulk copies (global <-> shared), e.g. token rows for dispatch/combine.
+// The global side may be an NVLink-mapped peer address.
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(dst), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int32_t c0, int32_t c1) {

@@ -84,7 +84,7 @@ def s_index():
             ctx.close()
 
 
-def run_layer(E, topk, N, K, M, std=0.0, act=None, weighted=False, n_comm1=2, wave=4, group=16,
+def run_layer(E, topk, N, K, M, std=0.0, act=None, weighted=False, n_comm1=0, wave=4, group=16,
               seed=0, timing=False):
     model = C.ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
     r = Rt.build_routing(model, C.ParallelSpec(1, 1), C.WorkloadSpec(M=M, seed=seed, std=std))
@@ -99,20 +99,20 @@ def run_layer(E, topk, N, K, M, std=0.0, act=None, weighted=False, n_comm1=2, wa
     ctx.token_buffer()[:M].copy_(x)
     y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     a = _lib.ACTIVATIONS[act]
-    ctx.forward(ex, M, w0t, w1t, cw, y, activation=a, n_comm0=0, n_comm1=n_comm1, group0=group, wave1=wave)
+    ctx.forward(ex, M, w0t, w1t, cw, y, activation=a, n_comm0=n_comm1, n_comm1=n_comm1, group0=group, wave1=wave)
     torch.cuda.synchronize()
     ref = torch_ref(x, w0, w1, ex.long(), act, cw)
     mx, fr = O.relative_error(y.float().cpu().numpy(), ref.cpu().numpy())
     print(f"    E{E} top{topk} N{N} K{K} M{M} act={act} w={weighted}: max/max={mx:.2e} frob={fr:.2e}")
     if timing:
         for _ in range(3):
-            ctx.forward(ex, M, w0t, w1t, cw, y, activation=a, n_comm0=0, n_comm1=n_comm1, group0=group, wave1=wave)
+            ctx.forward(ex, M, w0t, w1t, cw, y, activation=a, n_comm0=n_comm1, n_comm1=n_comm1, group0=group, wave1=wave)
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         n = 10
         st.record()
         for _ in range(n):
-            ctx.forward(ex, M, w0t, w1t, cw, y, activation=a, n_comm0=0, n_comm1=n_comm1, group0=group, wave1=wave)
+            ctx.forward(ex, M, w0t, w1t, cw, y, activation=a, n_comm0=n_comm1, n_comm1=n_comm1, group0=group, wave1=wave)
         en.record()
         torch.cuda.synchronize()
         ms = st.elapsed_time(en) / n
@@ -145,11 +145,18 @@ def s_mx_small():
 @stage("layer EP=1 Mixtral M=8192")
 def s_mx():
     run_layer(8, 2, 4096, 14336, 8192, timing=True)
+    run_layer(8, 2, 4096, 14336, 8192, timing=True, n_comm1=4)
+
+
+@stage("layer EP=1 comm-CTA combine, tanh weighted")
+def s_comm():
+    run_layer(8, 3, 512, 1024, 1000, act="tanh", weighted=True, n_comm1=2)
+    run_layer(8, 2, 4096, 14336, 1024, std=0.05, weighted=True, n_comm1=6)
 
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["info", "index", "small", "small2", "c1", "mxs", "mx"]
     table = {"info": s_info, "index": s_index, "small": s_small, "small2": s_small2, "c1": s_c1,
-             "mxs": s_mx_small, "mx": s_mx}
+             "mxs": s_mx_small, "mx": s_mx, "comm": s_comm}
     for w in which:
         table[w]()
