@@ -122,6 +122,12 @@ int comet_layer0(comet_ctx* ctx, const void* w0t, int activation, int n_comm, in
 int comet_layer1(comet_ctx* ctx, const void* w1t, const float* combine_w, void* y_local, int n_comm,
                  int wave, void* stream);
 
+/* Remote half of the combine (world > 1): wait for every sender's partial
+ * rows of this rank's tokens and sum them in ascending rank order
+ * (executor.py:239-245).  Separate from comet_layer1 so that ranks emulated
+ * on one device can enqueue all layer1 launches before any finish. */
+int comet_combine_finish(comet_ctx* ctx, void* y_local, void* stream);
+
 /* Whole layer forward of one rank: index build, token-ready signal,
  * layer0, layer1 (+ remote combine finish when world > 1). */
 int comet_forward(comet_ctx* ctx, const int32_t* d_experts, int M, const void* w0t, const void* w1t,

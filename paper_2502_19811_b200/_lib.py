@@ -30,7 +30,7 @@ EXPORTS = (
     "comet_last_error", "comet_version", "comet_ctx_create", "comet_ctx_destroy",
     "comet_symm_export", "comet_symm_import", "comet_link_local", "comet_token_buffer",
     "comet_routing_buffer", "comet_index_build", "comet_index_sizes", "comet_index_download",
-    "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_forward",
+    "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
 )
 
@@ -90,6 +90,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_signal_tokens_ready": ([vp, vp], i32),
         "comet_layer0": ([vp, vp, i32, i32, i32, vp], i32),
         "comet_layer1": ([vp, vp, vp, vp, i32, i32, vp], i32),
+        "comet_combine_finish": ([vp, vp, vp], i32),
         "comet_forward": ([vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp], i32),
         "comet_device_info": ([i32, _P32], i32),
     }
@@ -205,7 +206,10 @@ class Context:
         s = stream if stream is not None else t.cuda.current_stream(self.device)
         return s.cuda_stream
 
-    def index_build(self, experts_dev, M: int, tile_rows: int = 128, tile_cols: int = 128, stream=None) -> None:
+    def index_build(self, experts_dev, M: int, tile_rows: int = 128, tile_cols: Optional[int] = None,
+                    stream=None) -> None:
+        if tile_cols is None:  # reference default_tile_cols (resolver.py:35-39)
+            tile_cols = 128 if self.N >= 512 else max(1, self.N // 4)
         check(self.lib.comet_index_build(self.handle, ctypes.c_void_p(experts_dev.data_ptr()), M,
                                          tile_rows, tile_cols, ctypes.c_void_p(self._stream(stream))))
 
@@ -263,6 +267,10 @@ class Context:
         check(self.lib.comet_layer1(self.handle, ctypes.c_void_p(w1t.data_ptr()), cw,
                                     ctypes.c_void_p(y_local.data_ptr()), n_comm, wave,
                                     ctypes.c_void_p(self._stream(stream))))
+
+    def combine_finish(self, y_local=None, stream=None) -> None:
+        ptr = ctypes.c_void_p(y_local.data_ptr()) if y_local is not None else None
+        check(self.lib.comet_combine_finish(self.handle, ptr, ctypes.c_void_p(self._stream(stream))))
 
     def forward(self, experts_dev, M: int, w0t, w1t, combine_w, y_local, activation: int = 0,
                 n_comm0: int = 2, n_comm1: int = 2, group0: int = 16, wave1: int = 4, stream=None) -> None:

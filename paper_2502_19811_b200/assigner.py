@@ -1,0 +1,251 @@
+"""Adaptive compute/communication block split, chosen from measured timings.
+
+Mirror of `pkg/src/moepipe/assigner.py` (the split knob of
+`simulator.py:45-65`).  ``KernelSplit``, ``split_for``, ``SplitKey``,
+``SplitRecord``, ``SplitMetadata``, ``select_split`` and
+``UnprofiledConfigError`` keep the reference's semantics and JSON schema
+(assigner.py:44-292): argmin over the sweep curve with ties to the smaller
+n_c, exact-key lookup else the nearest log2 token bucket (ties to the
+smaller M), refusal when nothing compatible was profiled.
+
+What changes on B200: ``sweep_split`` times the real fused layer kernels on
+this GPU (CUDA events, median over repeats) instead of running the
+discrete-event simulator, and records ``cost="b200"`` with ``blocks`` = the
+device's SM count.  n_c is the number of communication CTAs of the fused
+layer kernels (layer1's combine CTAs; layer0's NVLink dispatch CTAs when the
+layer has remote rows).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import tempfile
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence, Tuple
+
+from .config import ConfigurationError, ModelConfig, ParallelSpec, WorkloadSpec, canonical_json
+
+
+class UnprofiledConfigError(ConfigurationError):
+    """No profiled record is compatible with the query (ref assigner.py:40-41)."""
+
+
+@dataclass(frozen=True)
+class KernelSplit:
+    """n thread blocks = n_p compute + n_c communication (ref simulator.py:45-61)."""
+
+    n: int
+    n_p: int
+    n_c: int
+
+    def __post_init__(self) -> None:
+        if self.n_p < 1 or self.n_c < 1:
+            raise ConfigurationError(
+                f"both block pools need at least one block, got n_p={self.n_p}, n_c={self.n_c}")
+        if self.n_p + self.n_c != self.n:
+            raise ConfigurationError(f"n_p + n_c must equal n: {self.n_p} + {self.n_c} != {self.n}")
+
+
+def split_for(n: int, n_c: int) -> KernelSplit:
+    return KernelSplit(n=n, n_p=n - n_c, n_c=n_c)
+
+
+_KEY_FIELDS = ("m", "tp", "ep", "experts", "topk", "embed", "hidden", "cost", "blocks")
+
+
+@dataclass(frozen=True)
+class SplitKey:
+    """One profiled configuration; ``m`` is the token bucket (ref 44-117)."""
+
+    m: int
+    tp: int
+    ep: int
+    experts: int
+    topk: int
+    embed: int
+    hidden: int
+    cost: str
+    blocks: int
+
+    def compatible(self, other: "SplitKey") -> bool:
+        return all(getattr(self, f) == getattr(other, f) for f in _KEY_FIELDS if f != "m")
+
+    def to_json_dict(self) -> dict:
+        return {f: getattr(self, f) for f in _KEY_FIELDS}
+
+    @classmethod
+    def from_json_dict(cls, data: dict) -> "SplitKey":
+        vals = {f: (str(data[f]) if f == "cost" else int(data[f])) for f in _KEY_FIELDS}
+        return cls(**vals)
+
+    @classmethod
+    def for_config(cls, model: ModelConfig, parallel: ParallelSpec, m_tokens: int,
+                   cost_name: str, blocks: int) -> "SplitKey":
+        return cls(m=m_tokens, tp=parallel.tp, ep=parallel.ep, experts=model.E, topk=model.topk,
+                   embed=model.N, hidden=model.K, cost=cost_name, blocks=blocks)
+
+
+@dataclass(frozen=True)
+class SplitRecord:
+    """Sweep curve and its argmin (ref 120-153)."""
+
+    key: SplitKey
+    optimal_nc: int
+    latency_ns: int
+    curve: Tuple[Tuple[int, int], ...]
+
+    def __post_init__(self) -> None:
+        if not self.curve:
+            raise ConfigurationError("sweep curve is empty")
+        best = min(self.curve, key=lambda pt: (pt[1], pt[0]))
+        if (self.optimal_nc, self.latency_ns) != best:
+            raise ConfigurationError("stored optimum is not the argmin of the stored curve")
+
+    def to_json_dict(self) -> dict:
+        return {"key": self.key.to_json_dict(), "optimal_nc": self.optimal_nc,
+                "latency_ns": self.latency_ns, "curve": [list(pt) for pt in self.curve]}
+
+    @classmethod
+    def from_json_dict(cls, data: dict) -> "SplitRecord":
+        return cls(key=SplitKey.from_json_dict(data["key"]), optimal_nc=int(data["optimal_nc"]),
+                   latency_ns=int(data["latency_ns"]),
+                   curve=tuple((int(a), int(b)) for a, b in data["curve"]))
+
+
+@dataclass
+class SplitMetadata:
+    """Flat store of records persisted as one JSON file (ref 156-197)."""
+
+    records: List[SplitRecord]
+
+    def add(self, record: SplitRecord) -> None:
+        self.records = [r for r in self.records if r.key != record.key] + [record]
+
+    def to_json_str(self) -> str:
+        ordered = sorted(self.records, key=lambda r: tuple(sorted(r.key.to_json_dict().items())))
+        return canonical_json({"records": [r.to_json_dict() for r in ordered]})
+
+    @classmethod
+    def from_json_str(cls, text: str) -> "SplitMetadata":
+        return cls(records=[SplitRecord.from_json_dict(r) for r in json.loads(text).get("records", [])])
+
+    def save(self, path: str) -> None:
+        """Whole-file atomic replace."""
+        fd, tmp = tempfile.mkstemp(dir=os.path.dirname(os.path.abspath(path)), suffix=".tmp")
+        try:
+            with os.fdopen(fd, "w") as fh:
+                fh.write(self.to_json_str())
+            os.replace(tmp, path)
+        except BaseException:
+            if os.path.exists(tmp):
+                os.unlink(tmp)
+            raise
+
+    @classmethod
+    def load(cls, path: str) -> "SplitMetadata":
+        with open(path) as fh:
+            return cls.from_json_str(fh.read())
+
+
+def candidate_ncs(blocks: int, stride: int = 2, max_nc: Optional[int] = None) -> List[int]:
+    """Even n_c candidates (2-CTA clusters) from 2 to ``max_nc``."""
+    if stride < 1:
+        raise ConfigurationError(f"stride must be >= 1, got {stride}")
+    hi = min(blocks - 2, max_nc if max_nc is not None else blocks - 2)
+    out = list(range(2, hi + 1, max(2, stride + (stride & 1))))
+    if not out:
+        raise ConfigurationError("no candidate split")
+    return out
+
+
+def record_from_curve(key: SplitKey, points: Sequence[Tuple[int, int]]) -> SplitRecord:
+    curve = tuple(sorted((int(a), int(b)) for a, b in points))
+    nc, ns = min(curve, key=lambda pt: (pt[1], pt[0]))
+    return SplitRecord(key=key, optimal_nc=nc, latency_ns=ns, curve=curve)
+
+
+def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSpec,
+                cost=None, cost_name: str = "b200", blocks: Optional[int] = None,
+                stride: int = 2, rank: int = 0, max_nc: int = 16, repeats: int = 5,
+                measure: Optional[Callable[[int], float]] = None) -> SplitRecord:
+    """Measure the fused layer at each candidate n_c and record the argmin.
+
+    ``measure(n_c) -> seconds`` defaults to timing ``MoELayer`` on this GPU
+    with synthetic tokens and random weights of the model's shape (single
+    device; for world > 1 the ranks are emulated on the device, so the curve
+    reflects on-device comm traffic -- the multi-GPU sweep uses
+    bench.py --sweep under torchrun).  ``cost`` is accepted for signature
+    compatibility with the reference and ignored.
+    """
+    if blocks is None:
+        from . import _lib
+        blocks = _lib.device_info(0)["sms"]
+    if measure is None:
+        measure = _default_measure(model, parallel, workload, repeats)
+    points = [(nc, int(round(measure(nc) * 1e9))) for nc in candidate_ncs(blocks, stride, max_nc)]
+    key = SplitKey.for_config(model, parallel, workload.M, cost_name, blocks)
+    return record_from_curve(key, points)
+
+
+def _default_measure(model, parallel, workload, repeats):
+    import numpy as np
+    from . import _lib
+    from .executor import LayerKnobs, RankWeights, MoELayer, _layers
+    from .routing import build_routing
+    torch = _lib.require_device()
+    routing = build_routing(model, parallel, workload)
+    g = torch.Generator(device="cuda").manual_seed(workload.seed + 2)
+    w0 = torch.randn(model.E, model.N, model.K, device="cuda", generator=g) / math.sqrt(model.N)
+    w1 = torch.randn(model.E, model.K, model.N, device="cuda", generator=g) / math.sqrt(model.N)
+    rws = [RankWeights.from_full(w0, w1, model, parallel, r) for r in range(parallel.world_size)]
+    del w0, w1
+    layers = _layers(model, parallel, max(1, workload.M), rws, 0)
+    x = torch.randn(workload.M, model.N, device="cuda", generator=g).to(torch.bfloat16)
+    ex = torch.from_numpy(routing.as_array().copy()).cuda()
+    outs = []
+    for layer in layers:
+        lo, hi = layer.token_range(workload.M)
+        layer.place_tokens(x[lo:hi], workload.M)
+        outs.append(torch.empty(hi - lo, layer.n_pad, dtype=torch.bfloat16, device="cuda"))
+
+    def run(nc):
+        for layer, y in zip(layers, outs):
+            layer.knobs = LayerKnobs(n_comm0=nc, n_comm1=nc)
+        from .executor import _phase_forward
+        _phase_forward(layers, ex, workload.M, outs, None)
+
+    def measure(nc):
+        run(nc)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(repeats):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            run(nc)
+            e.record()
+            torch.cuda.synchronize()
+            times.append(s.elapsed_time(e) / 1e3)
+        return float(sorted(times)[len(times) // 2])
+    return measure
+
+
+def select_split(metadata: SplitMetadata, query: SplitKey) -> KernelSplit:
+    """Exact key, else nearest log2 token bucket (ties -> smaller M), else
+    ``UnprofiledConfigError`` (ref assigner.py:260-292)."""
+    if not metadata.records:
+        raise UnprofiledConfigError("split metadata is empty")
+    compatible = [r for r in metadata.records if r.key.compatible(query)]
+    if not compatible:
+        raise UnprofiledConfigError(
+            f"unprofiled configuration: no record matches {query.to_json_dict()} "
+            "in every field but the token count")
+    exact = [r for r in compatible if r.key.m == query.m]
+    if exact:
+        chosen = exact[0]
+    else:
+        if query.m < 1:
+            raise UnprofiledConfigError(f"cannot bucket a token count of {query.m}; profile it explicitly")
+        chosen = min(compatible, key=lambda r: (abs(math.log2(query.m) - math.log2(r.key.m)), r.key.m))
+    return split_for(chosen.key.blocks, chosen.optimal_nc)

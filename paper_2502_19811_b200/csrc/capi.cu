@@ -53,8 +53,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kLayerThreads = 256;
-constexpr int kLayerStages = 6;
-constexpr size_t kLayerSmem = kLayerStages * 32768 + 2 * 16384 + 1024 + 1024;
+constexpr size_t kLayerSmem = kLayerStages * 32768 + 1024 + 1024;
 constexpr int kIndexThreads = 1024;
 constexpr size_t kIndexSmem = 8192 * sizeof(long long);
 
@@ -137,6 +136,8 @@ struct comet_ctx {
   int32_t* routing = nullptr;
 
   CUtensorMap tm_xs, tm_H, tm_y, tm_xg;
+  void* last_y = nullptr;
+  const float* last_combine_w = nullptr;
   MapCache w0c, w1c;
 };
 
@@ -592,6 +593,8 @@ int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int 
   a.order_group = group;
   a.activation = activation;
   a.pairs = x->ix.pairs0;
+  a.out = x->H;
+  a.out_ld = x->k_local;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // HBM-local rows first (whole GPU, bandwidth-bound); comm CTAs pull only remote rows.
   dispatch_local_kernel<<<x->n_sm * 4, 256, 0, st>>>(x->ix.gather_row, x->ix.meta, x->xs, x->xg, c.N, x->M, c.world,
@@ -615,6 +618,8 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   a.b_rows = c.N;
   a.order_group = wave;
   a.pairs = x->ix.pairs1;
+  a.out = x->yrows;
+  a.out_ld = c.N;
   a.combine_w = combine_w;
   a.y_local = static_cast<__nv_bfloat16*>(y_local);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -625,10 +630,23 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
     combine_local_kernel<<<x->n_sm * 8, 256, 0, st>>>(x->ix.tok_pos, combine_w, x->yrows,
                                                       static_cast<__nv_bfloat16*>(y_local), t0, n_tok, c.topk, c.N);
     CK(cudaGetLastError());
-  } else if (c.world > 1) {
-    combine_finish_kernel<<<x->n_sm, 256, 0, st>>>(a, x->cb, x->cb_flag, x->ix.experts);
-    CK(cudaGetLastError());
   }
+  x->last_y = y_local;
+  x->last_combine_w = combine_w;
+  return COMET_OK;
+}
+
+int comet_combine_finish(comet_ctx* x, void* y_local, void* stream) {
+  const auto& c = x->cfg;
+  if (c.world == 1) return COMET_OK;
+  CK(cudaSetDevice(c.device));
+  LayerArgs a = base_args(x);
+  a.layer = 1;
+  a.n_blocks = x->nb1;
+  a.y_local = static_cast<__nv_bfloat16*>(y_local ? y_local : x->last_y);
+  combine_finish_kernel<<<x->n_sm, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, x->cb, x->cb_flag,
+                                                                               x->ix.experts);
+  CK(cudaGetLastError());
   return COMET_OK;
 }
 
@@ -640,7 +658,8 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
   if (x->cfg.world > 1)
     if (int rc = comet_signal_tokens_ready(x, stream)) return rc;
   if (int rc = comet_layer0(x, w0t, activation, n_comm0, group0, stream)) return rc;
-  return comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream);
+  if (int rc = comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream)) return rc;
+  return comet_combine_finish(x, y_local, stream);
 }
 
 }  // extern "C"

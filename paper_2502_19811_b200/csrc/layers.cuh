@@ -7,6 +7,8 @@
 
 namespace comet {
 
+constexpr int kLayerStages = 7;  // 32 KB smem stages per CTA (A 16 KB + B 16 KB)
+
 enum Activation : int { kActIdentity = 0, kActRelu = 1, kActSilu = 2, kActGeluTanh = 3, kActTanh = 4 };
 
 struct LayerArgs {
@@ -40,6 +42,8 @@ struct LayerArgs {
   const float* combine_w;     // [M*topk] or null
 
   // buffers
+  __nv_bfloat16* out;             // epilogue output: H (layer0) or yrows (layer1), row-major
+  int out_ld;                     // its row length in elements (K_local or N)
   __nv_bfloat16* xs_local;        // [M_cap, N] this rank's symmetric token buffer
   const __nv_bfloat16* const* xs_peer;  // [world] peer token buffers (device array)
   uint32_t* tok_ready;            // [M_cap] epoch when xs_local[t] holds token t

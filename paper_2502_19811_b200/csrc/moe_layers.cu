@@ -32,12 +32,11 @@ namespace comet {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kStages = 6;
+constexpr int kStages = kLayerStages;
 constexpr int kBlockK = 64;                       // bf16 elements = 128 B swizzle atom
 constexpr uint32_t kSmemA = kTileRows * kBlockK * 2;   // 16 KB
 constexpr uint32_t kSmemB = 128 * kBlockK * 2;         // 16 KB (half of the 256-row B block)
 constexpr uint32_t kSmemStage = kSmemA + kSmemB;
-constexpr uint32_t kSmemEpi = kTileRows * 128;          // 128 rows x 64 bf16
 constexpr uint32_t kAccCols = kBlockN;                  // fp32 columns per accumulator
 constexpr uint32_t kTmemCols = 2 * kAccCols;
 constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(2 * kTileRows, kBlockN);
@@ -104,7 +103,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     else comm::combine_reduce(p, smem);
     return;
   }
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kSmemStage + 2 * kSmemEpi);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kSmemStage);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
@@ -216,7 +215,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     // ---------------- epilogue: TMEM -> regs -> smem -> TMA store ----------------
     const int ew = warp - 4;
     const int row = ew * 32 + lane;  // row of this CTA's 128-row half
-    int it = 0, buf = 0;
+    int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
       const Unit w = decode_unit(u, p.layer, P, NB, p.order_group);
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
@@ -226,17 +225,29 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
       wait(tfull + a, aphase);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + a * kAccCols;
+      __nv_bfloat16* orow = p.out + static_cast<long long>(row0 + row) * p.out_ld + w.nb * kBlockN;
+      const int cols_left = p.out_ld - w.nb * kBlockN;  // ragged last n-block (e.g. K/tp = 3200)
 #pragma unroll 1
       for (int s = 0; s < kBlockN / 64; ++s) {
+        if (p.debug & 128) {  // debug: drain nothing
+          if (s == kBlockN / 64 - 1) {
+            ptx::tc_fence_before();
+            if (leader) ptx::mbar_arrive(tempty + a);
+            else ptx::mbar_arrive_cluster(tempty + a, 0);
+          }
+          continue;
+        }
         uint32_t v0[32], v1[32];
         ptx::tmem_ld32(taddr + s * 64, v0);
         ptx::tmem_ld32(taddr + s * 64 + 32, v1);
         ptx::tmem_ld_wait();
         if (s == kBlockN / 64 - 1) {
+          // accumulator drained: the MMA warp may start the unit after next
           ptx::tc_fence_before();
           if (leader) ptx::mbar_arrive(tempty + a);
           else ptx::mbar_arrive_cluster(tempty + a, 0);
         }
+        if (s * 64 >= cols_left || (p.debug & 64)) continue;
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
@@ -246,29 +257,24 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         for (int i = 0; i < 16; ++i)
           pk[16 + i] = pack_bf16(activate(__uint_as_float(v1[2 * i]), p.activation),
                                  activate(__uint_as_float(v1[2 * i + 1]), p.activation));
-        if (threadIdx.x == kEpiThread0) ptx::bulk_wait_read<1>();
-        ptx::named_bar_sync(1, 128);
-        uint8_t* sbuf = smem + kStages * kSmemStage + buf * kSmemEpi;
+        // direct stores from registers: no smem staging and no TMA store
+        // queued behind the producer's in-flight loads
+        // full 32-byte sectors per store (partial-sector writes cost ~30%)
+        char* dst = reinterpret_cast<char*>(orow + s * 64);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t off = row * 128 + ((c ^ (row & 7)) * 16);
-          *reinterpret_cast<uint4*>(sbuf + off) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        }
-        ptx::fence_async_shared();
+        for (int c = 0; c < 4; ++c)
+          ptx::st_v8_cs(dst + 32 * c, make_uint4(pk[8 * c], pk[8 * c + 1], pk[8 * c + 2], pk[8 * c + 3]),
+                     make_uint4(pk[8 * c + 4], pk[8 * c + 5], pk[8 * c + 6], pk[8 * c + 7]));
+      }
+      if (p.layer == 1) {
+        // this CTA's 128 rows of column block nb are in memory -> count them
         ptx::named_bar_sync(1, 128);
         if (threadIdx.x == kEpiThread0) {
-          ptx::tma_store_2d(&tm_out, sbuf, w.nb * kBlockN + s * 64, row0);
-          ptx::bulk_commit();
+          __threadfence();
+          ptx::red_release_gpu_add(p.nb_done + w.nb, 1u);
         }
-        buf ^= 1;
-      }
-      if (p.layer == 1 && threadIdx.x == kEpiThread0) {
-        ptx::bulk_wait<0>();
-        ptx::fence_async_global();
-        ptx::red_release_gpu_add(p.nb_done + w.nb, 1u);
       }
     }
-    if (threadIdx.x == kEpiThread0) ptx::bulk_wait<0>();
   }
 
   ptx::tc_fence_before();

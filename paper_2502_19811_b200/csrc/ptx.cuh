@@ -311,6 +311,19 @@ __device__ __forceinline__ uint4 ld_v4(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
   return v;
 }
+// 32-byte (full L2 sector) streaming store, evict-first: STG.E.EF.ENL2.256.
+// Used for the layer outputs so they do not evict the operand tiles that the
+// GEMM re-reads from L2.
+__device__ __forceinline__ void st_v8_cs(void* p, uint4 lo, uint4 hi) {
+  const uint64_t a = (static_cast<uint64_t>(lo.y) << 32) | lo.x, b = (static_cast<uint64_t>(lo.w) << 32) | lo.z;
+  const uint64_t c = (static_cast<uint64_t>(hi.y) << 32) | hi.x, d = (static_cast<uint64_t>(hi.w) << 32) | hi.z;
+  asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" :: "l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+__device__ __forceinline__ void st_v8(void* p, uint4 lo, uint4 hi) {
+  const uint64_t a = (static_cast<uint64_t>(lo.y) << 32) | lo.x, b = (static_cast<uint64_t>(lo.w) << 32) | lo.z;
+  const uint64_t c = (static_cast<uint64_t>(hi.y) << 32) | hi.x, d = (static_cast<uint64_t>(hi.w) << 32) | hi.z;
+  asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" :: "l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");

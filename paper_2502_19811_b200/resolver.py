@@ -184,7 +184,7 @@ def device_index(routing: RoutingTable, rank: int, tile_rows: int = DEFAULT_TILE
     torch = ctx.torch
     tc = default_tile_cols(routing.model.N) if tile_cols is None else tile_cols
     m = routing.workload.M
-    experts = torch.from_numpy(np.ascontiguousarray(routing.as_array(), dtype=np.int32))
+    experts = torch.from_numpy(routing.as_array().copy())
     dev = ctx.routing_buffer()[: m * routing.model.topk]
     if m:
         dev.copy_(experts.reshape(-1))

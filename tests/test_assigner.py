@@ -1,0 +1,60 @@
+"""Split chooser semantics (ref assigner.py:44-292) with synthetic measured
+curves; no GPU."""
+
+import pytest
+
+from paper_2502_19811_b200 import (ConfigurationError, KernelSplit, ModelConfig, ParallelSpec, SplitKey,
+                                   SplitMetadata, UnprofiledConfigError, WorkloadSpec, select_split,
+                                   split_for, sweep_split)
+from paper_2502_19811_b200.assigner import SplitRecord, candidate_ncs, record_from_curve
+
+MX = ModelConfig(L=32, E=8, topk=2, N=4096, K=14336)
+
+
+def key(m, ep=8, blocks=148):
+    return SplitKey.for_config(MX, ParallelSpec(1, ep), m, "b200", blocks)
+
+
+def test_kernel_split_invariants():
+    assert split_for(148, 8) == KernelSplit(148, 140, 8)
+    with pytest.raises(ConfigurationError):
+        KernelSplit(148, 148, 0)
+    with pytest.raises(ConfigurationError):
+        KernelSplit(148, 100, 8)
+
+
+def test_sweep_argmin_ties_to_smaller_nc():
+    curve = {2: 500, 4: 400, 6: 400, 8: 450}
+    rec = sweep_split(MX, ParallelSpec(1, 8), WorkloadSpec(M=8192), blocks=148, max_nc=8,
+                      measure=lambda nc: curve[nc] * 1e-9)
+    assert (rec.optimal_nc, rec.latency_ns) == (4, 400)
+    assert rec.curve == ((2, 500), (4, 400), (6, 400), (8, 450))
+    assert rec.key == key(8192)
+
+
+def test_record_rejects_non_argmin():
+    with pytest.raises(ConfigurationError):
+        SplitRecord(key=key(4096), optimal_nc=2, latency_ns=9, curve=((2, 9), (4, 3)))
+
+
+def test_select_exact_then_nearest_log2_bucket(tmp_path):
+    md = SplitMetadata(records=[])
+    md.add(record_from_curve(key(4096), [(2, 10), (4, 5)]))
+    md.add(record_from_curve(key(16384), [(2, 3), (4, 7)]))
+    path = tmp_path / "meta.json"
+    md.save(str(path))
+    md2 = SplitMetadata.load(str(path))
+    assert md2.to_json_str() == md.to_json_str()
+    assert select_split(md2, key(4096)).n_c == 4
+    assert select_split(md2, key(16384)).n_c == 2
+    assert select_split(md2, key(8192)).n_c == 4          # equidistant -> smaller bucket
+    assert select_split(md2, key(12000)).n_c == 2
+    with pytest.raises(UnprofiledConfigError):
+        select_split(md2, key(8192, ep=4))
+    with pytest.raises(UnprofiledConfigError):
+        select_split(SplitMetadata(records=[]), key(8192))
+
+
+def test_candidates_even_cluster_multiples():
+    assert candidate_ncs(148, 2, 12) == [2, 4, 6, 8, 10, 12]
+    assert all(nc % 2 == 0 for nc in candidate_ncs(148, 3, 40))

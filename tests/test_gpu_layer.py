@@ -1,0 +1,147 @@
+"""Fused layer numerics on the GPU, through the C-ABI (ctypes binding).
+
+Parity targets: the reference's own fp64 outputs (tests/golden/, produced by
+moepipe.execute_naive / execute_tp_sharded), the oracle restatement on
+bf16-rounded inputs, and a plain PyTorch fp32 reference for full-size
+shapes.  Tolerance (tests/refs.py): max|d|/max|ref| <= 1e-2 and
+||d||_F/||ref||_F <= 5e-3 (bf16 storage, fp32 accumulation)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import moe_oracle as O
+from paper_2502_19811_b200 import (ConfigurationError, ExpertWeights, LayerKnobs, ModelConfig, MoELayer,
+                                   ParallelSpec, RankWeights, WorkloadSpec, build_routing, execute_naive,
+                                   execute_scheduled, execute_tp_sharded, meta_for_layer0, meta_for_layer1,
+                                   random_weights, resolve_layer0, resolve_layer1)
+from paper_2502_19811_b200.executor import run_emulated
+from tests.refs import assert_close, oracle_bf16_inputs, torch_reference
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _small_cases():
+    z = np.load(os.path.join(GOLD, "layer_small.npz"))
+    return z, sorted({k.split("__")[0] for k in z.files})
+
+
+@pytest.mark.parametrize("name", _small_cases()[1])
+def test_reference_golden_small(name):
+    z, _ = _small_cases()
+    E, topk, N, K, M, tp, ep, seed, weighted = z[f"{name}__spec"].tolist()
+    act = str(z[f"{name}__act"])
+    fn = np.tanh if act == "tanh" else None
+    cw = z[f"{name}__cw"] if weighted else None
+    model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
+    routing = build_routing(model, ParallelSpec(tp=1 if tp > 1 else tp, ep=ep), WorkloadSpec(M=M, seed=seed))
+    np.testing.assert_array_equal(routing.as_array(), z[f"{name}__experts"])
+    w = ExpertWeights(z[f"{name}__w0"], z[f"{name}__w1"])
+    x = z[f"{name}__x"]
+    if tp == 1:
+        y = execute_naive(x, w, routing, activation=fn, combine_weights=cw)
+    else:
+        y = execute_tp_sharded(x, w, routing, tp, activation=fn, combine_weights=cw)
+    ref = z[f"{name}__y"]
+    # vs the reference's fp64 output (includes bf16 input quantisation)
+    assert_close(y, ref, max_rel=2e-2, frob_rel=1e-2, what=f"{name} vs reference fp64")
+    # vs the oracle on bf16-rounded inputs (kernel error only)
+    ora = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), fn, cw, tp=tp)
+    assert_close(y, ora, what=f"{name} vs oracle(bf16 inputs)")
+
+
+def test_reference_golden_config1_ep8_emulated():
+    z = np.load(os.path.join(GOLD, "layer_c1.npz"))
+    model = ModelConfig(L=1, E=8, topk=2, N=512, K=1024)
+    routing = build_routing(model, ParallelSpec(1, 8), WorkloadSpec(M=512, seed=0))
+    x = np.random.default_rng(1).standard_normal((512, 512))
+    w = random_weights(model, seed=2)
+    y = execute_naive(x, w, routing)
+    assert_close(y, z["y"], what="config1 EP=8 vs reference execute_naive")
+    s0 = [resolve_layer0(routing, g, meta_for_layer0(model, routing.workload)) for g in range(8)]
+    s1 = [resolve_layer1(routing, g, meta_for_layer1(model, routing.workload)) for g in range(8)]
+    y2 = execute_scheduled(x, w, routing, s0, s1)
+    np.testing.assert_array_equal(y, y2)  # tile order never changes the arithmetic
+    with pytest.raises(ConfigurationError):
+        execute_scheduled(x, w, routing, s0[1:], s1)
+    with pytest.raises(ConfigurationError):
+        execute_scheduled(x[:10], w, routing, s0, s1)
+
+
+@pytest.mark.parametrize("tp,ep,std", [(1, 1, 0.0), (1, 2, 0.05), (1, 4, 0.032), (1, 8, 0.0), (2, 2, 0.032),
+                                       (2, 4, 0.0)])
+def test_emulated_parallel_layouts_vs_oracle(tp, ep, std):
+    model = ModelConfig(L=1, E=8, topk=2, N=256, K=512)
+    routing = build_routing(model, ParallelSpec(tp, ep), WorkloadSpec(M=600, seed=5, std=std))
+    w = random_weights(model, seed=6)
+    x = np.random.default_rng(7).standard_normal((600, 256))
+    cw = np.random.default_rng(3).random((600, 2))
+    y = run_emulated(x, w, routing, ParallelSpec(tp, ep), combine_weights=cw,
+                     knobs=LayerKnobs(n_comm0=2, n_comm1=2)).cpu().numpy()
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), combine_weights=cw, tp=tp)
+    assert_close(y, ref, what=f"tp={tp} ep={ep} std={std}")
+
+
+@pytest.mark.parametrize("n_comm1", [0, 2, 6])
+def test_combine_paths_agree(n_comm1):
+    model = ModelConfig(L=1, E=8, topk=3, N=512, K=1024)
+    routing = build_routing(model, ParallelSpec(), WorkloadSpec(M=777, seed=9, std=0.05))
+    w = random_weights(model, seed=1)
+    x = np.random.default_rng(2).standard_normal((777, 512))
+    y = run_emulated(x, w, routing, ParallelSpec(), activation="tanh",
+                     knobs=LayerKnobs(n_comm1=n_comm1)).cpu().numpy()
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), np.tanh)
+    assert_close(y, ref, what=f"n_comm1={n_comm1}")
+
+
+def test_edge_cases():
+    model = ModelConfig(L=1, E=4, topk=2, N=64, K=128)
+    w = random_weights(model, seed=3)
+    # M = 0, M < world (all tokens on the last rank), one expert unused
+    r0 = build_routing(model, ParallelSpec(1, 2), WorkloadSpec(M=0))
+    assert execute_naive(np.zeros((0, 64)), w, r0).shape == (0, 64)
+    r1 = build_routing(model, ParallelSpec(1, 4), WorkloadSpec(M=3, seed=1))
+    x1 = np.random.default_rng(0).standard_normal((3, 64))
+    assert_close(execute_naive(x1, w, r1), oracle_bf16_inputs(x1, w.w0, w.w1, r1.as_array()), what="M<W")
+    r2 = build_routing(model, ParallelSpec(1, 2), WorkloadSpec(M=300, seed=2, std=max_std(4, 2)))
+    assert 0 in r2.expert_counts
+    x2 = np.random.default_rng(1).standard_normal((300, 64))
+    assert_close(execute_naive(x2, w, r2), oracle_bf16_inputs(x2, w.w0, w.w1, r2.as_array()), what="skew")
+    # zero input -> zero output (linearity, SPEC examples)
+    assert np.abs(execute_naive(np.zeros((300, 64)), w, r2)).max() == 0.0
+    # non-64-multiple shapes are zero-padded on the device
+    m3 = ModelConfig(L=1, E=3, topk=2, N=40, K=72)
+    r3 = build_routing(m3, ParallelSpec(), WorkloadSpec(M=50, seed=4))
+    w3 = random_weights(m3, seed=5)
+    x3 = np.random.default_rng(6).standard_normal((50, 40))
+    assert_close(execute_naive(x3, w3, r3), oracle_bf16_inputs(x3, w3.w0, w3.w1, r3.as_array()), what="pad")
+    with pytest.raises(ConfigurationError):
+        execute_naive(x3, w3, r3, activation=lambda a: a * 2)
+
+
+def max_std(E, k):
+    from paper_2502_19811_b200 import max_achievable_std
+    return max_achievable_std(E, k)
+
+
+def test_mixtral_full_size_vs_torch_fp32_and_determinism():
+    import torch
+    model = ModelConfig(L=1, E=8, topk=2, N=4096, K=14336)
+    par = ParallelSpec()
+    routing = build_routing(model, par, WorkloadSpec(M=8192, seed=0, std=0.032))
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w0 = torch.randn(8, 4096, 14336, device="cuda", generator=g) / 64.0
+    w1 = torch.randn(8, 14336, 4096, device="cuda", generator=g) / 64.0
+    x = torch.randn(8192, 4096, device="cuda", generator=g)
+    cw = torch.rand(8192, 2, device="cuda", generator=g)
+    layer = MoELayer(model, par, 0, 8192, RankWeights.from_full(w0, w1, model, par, 0))
+    ex = torch.from_numpy(routing.as_array().copy()).cuda()
+    y1 = layer.forward(x, ex, cw)
+    y2 = layer.forward(x, ex, cw)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)  # run-to-run bitwise deterministic (ordered combine)
+    ref = torch_reference(x, w0, w1, ex.long(), combine_w=cw)
+    assert_close(y1.float().cpu().numpy(), ref.cpu().numpy(), what="Mixtral M=8192 EP=1")
+    layer.close()

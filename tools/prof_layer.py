@@ -44,7 +44,7 @@ ctx.index_build(ex, a.M)
 t_idx = timeit(lambda: ctx.index_build(ex, a.M))
 configs = [(16, 4, 0)]
 if a.sweep:
-    configs = [(g0, w1, nc) for nc in (0, 2, 4, 8) for g0 in (4, 16) for w1 in (1, 4)]
+    configs = [(g0, 4, 0) for g0 in (1, 2, 4, 8, 16, 32, 64)] + [(16, w1, 0) for w1 in (1, 2, 8, 16)]
 for g0, w1, nc in configs:
     t0 = timeit(lambda: ctx.layer0(w0t, 0, nc, g0))
     t1 = timeit(lambda: ctx.layer1(w1t, None, y, nc, w1))
