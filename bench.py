@@ -315,6 +315,25 @@ def run_ours(args):
     h2d = x_host.numel() * 2 + ex_host.numel() * 4
     d2h = y_host.numel() * 2
 
+    # ---- unfused comparison path: NCCL all-to-all + cuBLAS grouped GEMM ----
+    unfused_ms = None
+    if tp == 1 and not args.no_unfused:
+        from paper_2502_19811_b200.unfused import UnfusedLayer
+        ul = UnfusedLayer(model, par, rank, layer.weights.w0t[:, :kl, :N].transpose(1, 2).contiguous(),
+                          layer.weights.w1t[:, :N, :kl].transpose(1, 2).contiguous())
+        for _ in range(3):
+            ul.forward(x_local, ex, M=M)
+        barrier(world)
+        s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_u = max(5, args.steps // 4)
+        s3.record(stream)
+        for _ in range(n_u):
+            ul.forward(x_local, ex, M=M)
+        e3.record(stream)
+        barrier(world)
+        unfused_ms = max_over_ranks(s3.elapsed_time(e3) / n_u, world)
+        del ul
+
     # ---- roofline ----
     peak_tf, hbm_gbs, peak_src = load_peaks()
     rows_max = max_over_ranks(float(rows), world)
@@ -345,6 +364,8 @@ def run_ours(args):
                          "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic, "peak_source": peak_src,
                          "flops_per_launch": flops_layer, "ms_per_launch": round(t_dom, 4)},
             "kernels_ms": {"layer0": round(t_l0, 4), "layer1": round(t_l1, 4)},
+            "unfused_ms": None if unfused_ms is None else round(unfused_ms, 4),
+            "speedup_vs_unfused": None if unfused_ms is None else round(unfused_ms / ms, 3),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
@@ -388,6 +409,7 @@ def main():
     ap.add_argument("--wave1", type=int, default=4)
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-unfused", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -139,6 +139,14 @@ void* comet_hidden_buffer(comet_ctx* ctx);   /* H [rows_pad_cap, K/tp] bf16 */
 void* comet_yrows_buffer(comet_ctx* ctx);    /* layer1 rows [rows_pad_cap, N] bf16 */
 int32_t comet_hidden_rows_cap(comet_ctx* ctx);
 
+/* Per-CTA timeline of the layer kernels (globaltimer ns): `cap` records per
+ * CTA and role (load, mma, tmem-wait, epilogue, comm); 0 disables.  dump
+ * copies n_sm * 5 * cap * 2 uint64 {start, (task+1) << 40 | duration} and
+ * clears the buffer (synchronises the device).  The Python side exports it
+ * in the reference simulator's timeline CSV schema (simulator.py:235-245). */
+int comet_timeline_enable(comet_ctx* ctx, int cap);
+int comet_timeline_dump(comet_ctx* ctx, void* host_buf, size_t cap_bytes);
+
 /* Number of SMs and max co-resident 2-CTA clusters for the layer kernel. */
 int comet_device_info(int device, int32_t out[4]);
 

@@ -32,7 +32,9 @@ EXPORTS = (
     "comet_routing_buffer", "comet_index_build", "comet_index_sizes", "comet_index_download",
     "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
+    "comet_timeline_enable", "comet_timeline_dump",
 )
+ROLES = ("load", "mma", "tmem_wait", "epilogue", "comm")
 
 
 class NativeUnavailable(RuntimeError):
@@ -93,6 +95,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_combine_finish": ([vp, vp, vp], i32),
         "comet_forward": ([vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp], i32),
         "comet_device_info": ([i32, _P32], i32),
+        "comet_timeline_enable": ([vp, i32], i32),
+        "comet_timeline_dump": ([vp, vp, c.c_size_t], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -267,6 +271,24 @@ class Context:
         check(self.lib.comet_layer1(self.handle, ctypes.c_void_p(w1t.data_ptr()), cw,
                                     ctypes.c_void_p(y_local.data_ptr()), n_comm, wave,
                                     ctypes.c_void_p(self._stream(stream))))
+
+    def timeline_enable(self, cap: int) -> None:
+        self._tl_cap = cap
+        check(self.lib.comet_timeline_enable(self.handle, cap))
+
+    def timeline_dump(self):
+        """[(cta, role, task, start_ns, end_ns)] of the launches since enable/dump."""
+        sms = device_info(self.device)["sms"]
+        n = sms * len(ROLES) * self._tl_cap * 2
+        buf = np.zeros(n, dtype=np.uint64)
+        check(self.lib.comet_timeline_dump(self.handle, buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes))
+        rec = buf.reshape(sms, len(ROLES), self._tl_cap, 2)
+        out = []
+        cta, role, idx = np.nonzero(rec[..., 1])
+        for c, r, i in zip(cta.tolist(), role.tolist(), idx.tolist()):
+            start, packed = int(rec[c, r, i, 0]), int(rec[c, r, i, 1])
+            out.append((c, ROLES[r], (packed >> 40) - 1, start, start + (packed & ((1 << 40) - 1))))
+        return out
 
     def combine_finish(self, y_local=None, stream=None) -> None:
         ptr = ctypes.c_void_p(y_local.data_ptr()) if y_local is not None else None

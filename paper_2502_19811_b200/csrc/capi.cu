@@ -53,7 +53,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kLayerThreads = 256;
-constexpr size_t kLayerSmem = kLayerStages * 32768 + 1024 + 1024;
+constexpr size_t kLayerSmem = kLayerStages * 49152 + 32768 + 1024 + 1024;
 constexpr int kIndexThreads = 1024;
 constexpr size_t kIndexSmem = 8192 * sizeof(long long);
 
@@ -136,6 +136,8 @@ struct comet_ctx {
   int32_t* routing = nullptr;
 
   CUtensorMap tm_xs, tm_H, tm_y, tm_xg;
+  unsigned long long* timeline = nullptr;
+  int timeline_cap = 0;
   void* last_y = nullptr;
   const float* last_combine_w = nullptr;
   MapCache w0c, w1c;
@@ -298,6 +300,7 @@ int comet_ctx_destroy(comet_ctx* x) {
   cudaFree(x->yrows);
   cudaFree(x->xg);
   cudaFree(x->xg_ready);
+  cudaFree(x->timeline);
   cudaFree(x->counters);
   cudaFree(x->routing);
   delete x;
@@ -549,6 +552,8 @@ static LayerArgs base_args(comet_ctx* x) {
   a.nb_done = x->counters;
   a.nb_sent = x->counters + x->nb1;
   a.mloc_cap = x->mloc_cap;
+  a.timeline = x->timeline;
+  a.timeline_cap = x->timeline_cap;
   return a;
 }
 
@@ -617,6 +622,7 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   a.k_blocks = x->kb1;
   a.b_rows = c.N;
   a.order_group = wave;
+  a.order_group2 = 8;
   a.pairs = x->ix.pairs1;
   a.out = x->yrows;
   a.out_ld = c.N;
@@ -633,6 +639,30 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   }
   x->last_y = y_local;
   x->last_combine_w = combine_w;
+  return COMET_OK;
+}
+
+int comet_timeline_enable(comet_ctx* x, int cap) {
+  CK(cudaSetDevice(x->cfg.device));
+  cudaFree(x->timeline);
+  x->timeline = nullptr;
+  x->timeline_cap = 0;
+  if (cap <= 0) return COMET_OK;
+  const size_t bytes = (size_t)x->n_sm * kRoles * cap * 2 * sizeof(unsigned long long);
+  CK(cudaMalloc(&x->timeline, bytes));
+  CK(cudaMemset(x->timeline, 0, bytes));
+  x->timeline_cap = cap;
+  return COMET_OK;
+}
+
+int comet_timeline_dump(comet_ctx* x, void* host_buf, size_t cap_bytes) {
+  if (!x->timeline) return fail(COMET_EINVAL, "timeline not enabled");
+  const size_t bytes = (size_t)x->n_sm * kRoles * x->timeline_cap * 2 * sizeof(unsigned long long);
+  if (cap_bytes < bytes) return fail(COMET_EINVAL, "timeline buffer too small (%zu < %zu)", cap_bytes, bytes);
+  CK(cudaSetDevice(x->cfg.device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host_buf, x->timeline, bytes, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(x->timeline, 0, bytes));
   return COMET_OK;
 }
 

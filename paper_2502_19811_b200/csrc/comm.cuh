@@ -158,7 +158,7 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
 // output (world == 1) or push the partial row to the token's source rank.
 __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
   const int K = p.topk, N = p.n_embed, NB = p.n_blocks;
-  constexpr uint32_t kSeg = kBlockN * 2;  // 512 B of one expert row per column block
+  constexpr uint32_t kSeg = kBlockN * 2;  // 1 KB of one expert row per 512-column block
   const uint32_t slot_bytes = K * kSeg;
   const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / slot_bytes)) / kReducers * kReducers;
   comm_init(p, smem, n_slots);
@@ -223,36 +223,40 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
   const int me = warp - 1;
   int k = 0;
   for (int nb = 0; nb < NB; ++nb) {
-    const bool col_ok = nb * kBlockN + lane * 8 < N;
     for (int j = 0; j < jobs; ++j, ++k) {
       if (k % kReducers != me) continue;
       const int slot = k % n_slots;
       ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
       const JobDesc& d = cs->desc[slot];
-      float acc[8];
+      __nv_bfloat16* dst = d.dst;
+      float w[8];
+      for (int s = 0; s < K; ++s) w[s] = d.w[s];
+      uint4 o[kBlockN / 256];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = 0.f;
-      for (int s = 0; s < K; ++s) {
-        const float w = d.w[s];
-        if (w == 0.f) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(smem + slot * slot_bytes + s * kSeg + lane * 16);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+      for (int h = 0; h < static_cast<int>(kBlockN / 256); ++h) {  // lane covers 8 columns per 256
+        float acc[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float2 f = __bfloat1622float2(h[c]);
-          acc[2 * c] += f.x * w;
-          acc[2 * c + 1] += f.y * w;
+        for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+        for (int s = 0; s < K; ++s) {
+          if (w[s] == 0.f) continue;
+          const uint4 v =
+              *reinterpret_cast<const uint4*>(smem + slot * slot_bytes + s * kSeg + h * 512 + lane * 16);
+          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float2 f = __bfloat1622float2(hv[c]);
+            acc[2 * c] += f.x * w[s];
+            acc[2 * c + 1] += f.y * w[s];
+          }
         }
+        o[h].x = pack2(acc[0], acc[1]); o[h].y = pack2(acc[2], acc[3]);
+        o[h].z = pack2(acc[4], acc[5]); o[h].w = pack2(acc[6], acc[7]);
       }
-      __nv_bfloat16* dst = d.dst + lane * 8;
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(cs->empty + slot);
-      if (col_ok) {
-        uint4 o;
-        o.x = pack2(acc[0], acc[1]); o.y = pack2(acc[2], acc[3]);
-        o.z = pack2(acc[4], acc[5]); o.w = pack2(acc[6], acc[7]);
-        ptx::st_v4(dst, o);
-      }
+#pragma unroll
+      for (int h = 0; h < static_cast<int>(kBlockN / 256); ++h)
+        if (nb * kBlockN + h * 256 + lane * 8 < N) ptx::st_v4(dst + h * 256 + lane * 8, o[h]);
     }
     if (p.world > 1) {
       // all reducers of this CTA finished nb -> count the CTA; last CTA signals peers

@@ -9,7 +9,7 @@ namespace comet {
 
 constexpr int kTileRows = 128;   // reference DEFAULT_TILE_ROWS (resolver.py:32) = one CTA's rows
 constexpr int kPairRows = 256;   // rows per 2-CTA MMA pair (UMMA M = 256)
-constexpr int kBlockN = 256;     // output columns per work unit (UMMA N = 256)
+constexpr int kBlockN = 512;     // output columns per work unit (two UMMA N = 256 halves)
 constexpr int kMaxWorld = 64;
 
 // scalar slots in IndexDev::meta

@@ -59,6 +59,18 @@ __device__ __forceinline__ int block_scan(int v, int* ws, int* total) {
   return before;
 }
 
+// Warp-aggregated shared-memory increment: lanes hitting the same counter are
+// merged (match.any) so each distinct address takes one atomic per warp.
+// Routing is highly concentrated (8 experts, or a single transfer cell at
+// EP=1), so plain per-lane atomics serialise on a handful of addresses.
+__device__ __forceinline__ void warp_add(int* base, int idx, bool active) {
+  const unsigned act = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const unsigned peers = __match_any_sync(act, idx);
+  const int leader = __ffs(peers) - 1;
+  if ((threadIdx.x & 31) == leader) atomicAdd(base + idx, __popc(peers));
+}
+
 __device__ __forceinline__ int slot_of(const int32_t* row, int topk, int e) {
   for (int s = 0; s < topk; ++s)
     if (row[s] == e) return s;
@@ -86,7 +98,10 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   // -------- phase 0 (every CTA): global histogram + hosted offsets --------
   for (int e = tid; e < E; e += kThreads) s_cnt[e] = 0;
   __syncthreads();
-  for (int i = tid; i < M * K; i += kThreads) atomicAdd(&s_cnt[ix.experts[i]], 1);
+  for (int i0 = 0; i0 < M * K; i0 += kThreads) {
+    const int i = i0 + tid;
+    warp_add(s_cnt, i < M * K ? ix.experts[i] : 0, i < M * K);
+  }
   __syncthreads();
   if (tid == 0) {
     int o = 0, p = 0;
@@ -145,14 +160,15 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     for (int i = tid; i < W * W; i += kThreads) s_tr[i] = 0;
     __syncthreads();
     const int per_group = E / ix.ep;
-    for (int i = tid; i < M * K; i += kThreads) {
-      const int t = i / K, e = ix.experts[i];
+    for (int i0 = 0; i0 < M * K; i0 += kThreads) {
+      const int i = i0 + tid;
+      const bool ok = i < M * K;
+      const int t = ok ? i / K : 0, e = ok ? ix.experts[i] : 0;
       const int src = src_rank_of(t, M, W);
       const int g = e / per_group;
-      for (int d = g * ix.tp; d < (g + 1) * ix.tp; ++d) atomicAdd(&s_tr[src * W + d], 1);
-      if (e < ix.e_lo || e >= ix.e_lo + Er) ix.tok_pos[i] = -1;
+      for (int d = 0; d < ix.tp; ++d) warp_add(s_tr, src * W + g * ix.tp + d, ok);
+      if (ok && (e < ix.e_lo || e >= ix.e_lo + Er)) ix.tok_pos[i] = -1;
     }
-    for (int t = tid; t < M; t += kThreads) ix.first_key[t] = INT_MAX;
     for (int i = tid; i < ix.n_zero_words; i += kThreads) ix.zero_words[i] = 0u;
     __syncthreads();
     for (int i = tid; i < W * W; i += kThreads) ix.transfer[i] = s_tr[i];
@@ -323,46 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   }
   __syncthreads();
 
-  // ---- NVLink pull list: distinct remote tokens in first-demand order ----
   const int Rpad = s_pad[Er];
-  if (!ovf) {
-    for (int r = tid; r < Rpad; r += kThreads) ix.key_slot[r] = -1;
-    __syncthreads();
-    for (int r = tid; r < Rpad; r += kThreads) {
-      const int t = __ldcg(ix.gather_row + r);
-      if (t < 0 || src_rank_of(t, M, W) == ix.rank) continue;
-      // pair containing padded row r, and its claim rank
-      int lo = 0, hi = Er - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_pad[mid] <= r) lo = mid; else hi = mid - 1;
-      }
-      const int in_e = r - s_pad[lo];
-      const int pidx = s_p0[lo] + in_e / kPairRows;
-      const int key = __ldcg(ix.pair_key + pidx) * kPairRows + in_e % kPairRows;
-      atomicMin(ix.first_key + t, key);
-    }
-    __syncthreads();
-    __threadfence_block();
-    for (int t = tid; t < M; t += kThreads) {
-      const int k = __ldcg(ix.first_key + t);
-      if (k != INT_MAX) ix.key_slot[k] = t;
-    }
-    __syncthreads();
-    int running = 0;
-    for (int c0 = 0; c0 < Rpad; c0 += kThreads) {
-      const int k = c0 + tid;
-      const int t = k < Rpad ? __ldcg(ix.key_slot + k) : -1;
-      int tot;
-      const int pos = running + block_scan(t >= 0 ? 1 : 0, s_ws, &tot);
-      if (t >= 0) {
-        ix.pull_token[pos] = t;
-        ix.pull_src[pos] = src_rank_of(t, M, W);
-      }
-      running += tot;
-    }
-    if (tid == 0) s_misc[2] = running;
-  }
+  if (tid == 0) s_misc[2] = 0;  // pull list retired: remote rows are pulled per tile (comm.cuh)
   __syncthreads();
 
   // ---- combine token list: tokens with >=1 hosted expert, ascending ----

@@ -7,7 +7,9 @@
 
 namespace comet {
 
-constexpr int kLayerStages = 7;  // 32 KB smem stages per CTA (A 16 KB + B 16 KB)
+enum TimelineRole : int { kRoleLoad = 0, kRoleMma = 1, kRoleTmemWait = 2, kRoleEpilogue = 3, kRoleComm = 4, kRoles = 5 };
+
+constexpr int kLayerStages = 4;  // 48 KB smem stages per CTA (A 16 KB + two B halves 16 KB)
 
 enum Activation : int { kActIdentity = 0, kActRelu = 1, kActSilu = 2, kActGeluTanh = 3, kActTanh = 4 };
 
@@ -23,6 +25,7 @@ struct LayerArgs {
   int k_blocks;           // 64-wide contraction blocks
   int b_rows;             // weight rows per expert in the 2D B view
   int order_group;        // layer0: pairs per group; layer1: n-blocks per wave
+  int order_group2;       // layer1: pairs per group inside a wave
   int activation;
   uint32_t epoch;
   int debug;              // bit0: comm CTAs idle; bit1: layer0 A by 2D tile (no gather); bit2: spin waits
@@ -56,7 +59,8 @@ struct LayerArgs {
   uint32_t* nb_sent;              // [n_blocks] layer1 comm CTA completion counters
   int mloc_cap;                   // combine slots per sender
 
-  // per-CTA timeline (optional): [gridDim * cap] x (kind|task, start, end)
+  // per-CTA timeline (optional, null = off): record r of CTA c, role k lives
+  // at ((c * kRoles + k) * timeline_cap + r) * 2 as {start_ns, end_ns | tag}
   unsigned long long* timeline;
   int timeline_cap;
 };

@@ -31,26 +31,49 @@ namespace comet {
 
 namespace {
 
+// Work unit = 256 rows (a 2-CTA pair, 128 rows per CTA) x 512 output columns.
+// Each k-step issues two UMMA 256x256x16 (cta_group::2) that share the A tile
+// and use the two 256-column halves of the B block; both accumulators live in
+// TMEM (2 x 256 fp32 columns = all 512).  Per SM and k-element this moves
+// 128 A + 256 B rows for 128x512 MACs: 48 B/cycle at full rate instead of 64
+// for a 256x256 pair tile (the L2->SM traffic and the power that costs set the
+// sustained clock under the 1 kW cap).
 constexpr int kThreads = 256;
 constexpr int kStages = kLayerStages;
-constexpr int kBlockK = 64;                       // bf16 elements = 128 B swizzle atom
-constexpr uint32_t kSmemA = kTileRows * kBlockK * 2;   // 16 KB
-constexpr uint32_t kSmemB = 128 * kBlockK * 2;         // 16 KB (half of the 256-row B block)
-constexpr uint32_t kSmemStage = kSmemA + kSmemB;
-constexpr uint32_t kAccCols = kBlockN;                  // fp32 columns per accumulator
-constexpr uint32_t kTmemCols = 2 * kAccCols;
-constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(2 * kTileRows, kBlockN);
-constexpr int kEpiThread0 = 128;                        // first epilogue thread
+constexpr int kBlockK = 64;                              // bf16 elements = 128 B swizzle atom
+constexpr uint32_t kSmemA = kTileRows * kBlockK * 2;     // 16 KB: this CTA's 128 A rows
+constexpr uint32_t kSmemBh = 128 * kBlockK * 2;          // 16 KB: this CTA's 128 rows of one B half
+constexpr uint32_t kSmemStage = kSmemA + 2 * kSmemBh;    // 48 KB
+constexpr uint32_t kHalfN = kBlockN / 2;                 // 256 columns per UMMA / accumulator
+constexpr uint32_t kTmemCols = kBlockN;                  // 512 = both accumulators
+constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(2 * kTileRows, kHalfN);
+constexpr int kEpiThread0 = 128;                         // first epilogue thread
+constexpr uint32_t kSmemEpiWarp = 32 * 128;              // one warp's 32 rows x 64 columns (bf16)
+constexpr uint32_t kSmemEpi = 2 * 4 * kSmemEpiWarp;      // double-buffered, 4 epilogue warps
 
 struct Unit {
   int pair, nb;
 };
 
-// Unit u -> (pair, n-block).  layer0: groups of `G` pairs, n-block middle,
-// pair inner (weights block shared by the group, group's rows stay in L2);
-// layer1: waves of `G` n-blocks, pair outer, n-block inner (the reference's
-// column-wave order at wave granularity).
-__device__ __forceinline__ Unit decode_unit(int u, int layer, int P, int NB, int G) {
+// Timeline record: interval [t0, t1] of `role` for unit `task` on this CTA
+// (globaltimer ns).  Exported as the reference simulator's timeline CSV
+// (block_id, block_kind, task_id, start_ns, end_ns; simulator.py:235-245).
+__device__ __forceinline__ void tl_record(const LayerArgs& p, int role, int idx, int task, uint64_t t0, uint64_t t1) {
+  if (p.timeline == nullptr || idx >= p.timeline_cap) return;
+  unsigned long long* r = p.timeline + ((static_cast<long long>(blockIdx.x) * kRoles + role) * p.timeline_cap + idx) * 2;
+  r[0] = t0;
+  r[1] = (t1 - t0) | (static_cast<unsigned long long>(task + 1) << 40);
+}
+
+// Unit u -> (pair, n-block), L2-aware rasters.
+//  layer0: groups of G pairs; inside a group n-block middle, pair inner (the
+//          group's A rows stay in L2 across all n-blocks; each weight block is
+//          read once per group).
+//  layer1: waves of W n-blocks (the reference's column waves, resolver.py:
+//          273-296, at wave granularity: a wave's reduce chunks complete
+//          together); inside a wave, groups of G2 pairs, n-block middle,
+//          pair inner.
+__device__ __forceinline__ Unit decode_unit(int u, int layer, int P, int NB, int G, int G2) {
   Unit r;
   if (layer == 0) {
     const int per_group = G * NB;
@@ -66,28 +89,44 @@ __device__ __forceinline__ Unit decode_unit(int u, int layer, int P, int NB, int
     const int nb0 = w * G;
     const int we = min(G, NB - nb0);
     const int rem = u - w * per_wave;
-    r.pair = rem / we;
-    r.nb = nb0 + rem % we;
+    const int per_group = G2 * we;
+    const int g = rem / per_group;
+    const int base = g * G2;
+    const int ge = min(G2, P - base);
+    const int rem2 = rem - g * per_group;
+    r.nb = nb0 + rem2 / ge;
+    r.pair = base + rem2 % ge;
   }
   return r;
 }
 
-__device__ __forceinline__ float activate(float x, int act) {
-  switch (act) {
-    case kActRelu: return fmaxf(x, 0.f);
-    case kActSilu: return x / (1.f + __expf(-x));
-    case kActGeluTanh: {
-      const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-      return 0.5f * x * (1.f + tanhf(u));
-    }
-    case kActTanh: return tanhf(x);
-    default: return x;
-  }
+template <int ACT>
+__device__ __forceinline__ float activate(float x) {
+  if constexpr (ACT == kActRelu) return fmaxf(x, 0.f);
+  else if constexpr (ACT == kActSilu) return x / (1.f + __expf(-x));
+  else if constexpr (ACT == kActGeluTanh) {
+    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+    return 0.5f * x * (1.f + tanhf(u));
+  } else if constexpr (ACT == kActTanh) return tanhf(x);
+  else return x;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 64 fp32 accumulator columns -> activation -> 32 packed bf16 pairs.  The
+// activation is resolved once per chunk (a runtime switch per element costs a
+// jump-table branch per value).
+template <int ACT>
+__device__ __forceinline__ void pack_chunk(const uint32_t (&v0)[32], const uint32_t (&v1)[32], uint32_t (&pk)[32]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    pk[i] = pack_bf16(activate<ACT>(__uint_as_float(v0[2 * i])), activate<ACT>(__uint_as_float(v0[2 * i + 1])));
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    pk[16 + i] = pack_bf16(activate<ACT>(__uint_as_float(v1[2 * i])), activate<ACT>(__uint_as_float(v1[2 * i + 1])));
 }
 
 }  // namespace
@@ -103,12 +142,13 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     else comm::combine_reduce(p, smem);
     return;
   }
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kSmemStage);
+  uint8_t* epi_smem = smem + kStages * kSmemStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kSmemEpi);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
-  uint64_t* tfull = bars + 2 * kStages;
-  uint64_t* tempty = bars + 2 * kStages + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* tfull = bars + 2 * kStages;       // accumulators ready (one per unit)
+  uint64_t* tempty = bars + 2 * kStages + 1;  // [2]: accumulator half drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = blockIdx.x & 1;  // rank in the 2-CTA cluster
@@ -122,17 +162,15 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tm_a);
     ptx::prefetch_tmap(&tm_b);
-    ptx::prefetch_tmap(&tm_out);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(full + s, 2);
       ptx::mbar_init(empty + s, 1);
     }
-    for (int a = 0; a < 2; ++a) {
-      ptx::mbar_init(tfull + a, 1);
-      ptx::mbar_init(tempty + a, 2 * 128);
-    }
+    ptx::mbar_init(tfull, 1);
+    ptx::mbar_init(tempty + 0, 2 * 128);
+    ptx::mbar_init(tempty + 1, 2 * 128);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, kTmemCols);
@@ -151,8 +189,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     // ---------------- TMA producer ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = pair_id; u < U; u += n_pairs) {
-      const Unit w = decode_unit(u, p.layer, P, NB, p.order_group);
+    int it = 0;
+    for (int u = pair_id; u < U; u += n_pairs, ++it) {
+      const uint64_t t_start = ptx::globaltimer();
+      const Unit w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta);
@@ -171,15 +211,17 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           else ptx::mbar_arrive_cluster(full + stage, 0);
         } else if (lane == 0) {
           uint8_t* sa = smem + stage * kSmemStage;
-          uint8_t* sb = sa + kSmemA;
           ptx::tma_load_2d_2sm(sa, &tm_a, full + stage, kb * kBlockK, row0, ptx::kEvictNormal);
-          ptx::tma_load_2d_2sm(sb, &tm_b, full + stage, kb * kBlockK, brow, ptx::kEvictNormal);
+          ptx::tma_load_2d_2sm(sa + kSmemA, &tm_b, full + stage, kb * kBlockK, brow, ptx::kEvictNormal);
+          ptx::tma_load_2d_2sm(sa + kSmemA + kSmemBh, &tm_b, full + stage, kb * kBlockK, brow + kHalfN,
+                               ptx::kEvictNormal);
           if (leader) ptx::mbar_arrive_expect_tx(full + stage, 2 * kSmemStage);
           else ptx::mbar_arrive_cluster(full + stage, 0);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (lane == 0) tl_record(p, kRoleLoad, it, u, t_start, ptx::globaltimer());
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader CTA, one thread) ----------------
@@ -187,53 +229,67 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     uint32_t phase = 0;
     int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const int a = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
-      wait(tempty + a, aphase ^ 1);
+      const uint32_t ephase = (it & 1) ^ 1;  // previous unit's drain of each half
+      const uint64_t t_w = ptx::globaltimer();
+      wait(tempty + 0, ephase);
       ptx::tc_fence_after();
-      const uint32_t dcol = tmem_base + a * kAccCols;
+      const uint64_t t_m = ptx::globaltimer();
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         wait(full + stage, phase);
         ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint32_t sa = ptx::smem_u32(smem + stage * kSmemStage);
-          if (!(p.debug & 8)) {
-          const uint64_t da = ptx::sdesc_kmajor_sw128(sa);
-          const uint64_t db = ptx::sdesc_kmajor_sw128(sa + kSmemA);
+        const uint32_t sa = ptx::smem_u32(smem + stage * kSmemStage);
+        const uint64_t da = ptx::sdesc_kmajor_sw128(sa);
+        const uint64_t db0 = ptx::sdesc_kmajor_sw128(sa + kSmemA);
+        const uint64_t db1 = ptx::sdesc_kmajor_sw128(sa + kSmemA + kSmemBh);
+        // one fixed issuing lane: tcgen05.commit tracks the MMAs of its own thread
+        if (lane == 0 && !(p.debug & 8)) {
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
-            ptx::mma_bf16_2sm(dcol, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
+            ptx::mma_bf16_2sm(tmem_base, da + 2 * k, db0 + 2 * k, kIdesc, (kb | k) != 0);
+        }
+        __syncwarp();
+        if (kb == 0) {  // half 1 of the accumulator drains after half 0
+          wait(tempty + 1, ephase);
+          ptx::tc_fence_after();
+        }
+        if (lane == 0) {
+          if (!(p.debug & 8)) {
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k)
+              ptx::mma_bf16_2sm(tmem_base + kHalfN, da + 2 * k, db1 + 2 * k, kIdesc, (kb | k) != 0);
           }
           ptx::mma_commit_2sm(empty + stage, 0x3);
-          if (kb == p.k_blocks - 1) ptx::mma_commit_2sm(tfull + a, 0x3);
+          if (kb == p.k_blocks - 1) ptx::mma_commit_2sm(tfull, 0x3);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (lane == 0) {
+        tl_record(p, kRoleTmemWait, it, u, t_w, t_m);
+        tl_record(p, kRoleMma, it, u, t_m, ptx::globaltimer());
+      }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> regs -> smem -> TMA store ----------------
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
     const int ew = warp - 4;
-    const int row = ew * 32 + lane;  // row of this CTA's 128-row half
     int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const Unit w = decode_unit(u, p.layer, P, NB, p.order_group);
+      const Unit w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
-      const int a = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
-      wait(tfull + a, aphase);
+      wait(tfull, it & 1);
       ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + a * kAccCols;
-      __nv_bfloat16* orow = p.out + static_cast<long long>(row0 + row) * p.out_ld + w.nb * kBlockN;
+      const uint64_t t_e = ptx::globaltimer();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
       const int cols_left = p.out_ld - w.nb * kBlockN;  // ragged last n-block (e.g. K/tp = 3200)
 #pragma unroll 1
-      for (int s = 0; s < kBlockN / 64; ++s) {
+      for (int s = 0; s < static_cast<int>(kBlockN / 64); ++s) {
+        const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
         if (p.debug & 128) {  // debug: drain nothing
-          if (s == kBlockN / 64 - 1) {
+          if (half_end) {
             ptx::tc_fence_before();
-            if (leader) ptx::mbar_arrive(tempty + a);
-            else ptx::mbar_arrive_cluster(tempty + a, 0);
+            if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
+            else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
           }
           continue;
         }
@@ -241,30 +297,40 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         ptx::tmem_ld32(taddr + s * 64, v0);
         ptx::tmem_ld32(taddr + s * 64 + 32, v1);
         ptx::tmem_ld_wait();
-        if (s == kBlockN / 64 - 1) {
-          // accumulator drained: the MMA warp may start the unit after next
+        if (half_end) {
+          // accumulator half drained: the next unit's MMAs may overwrite it
           ptx::tc_fence_before();
-          if (leader) ptx::mbar_arrive(tempty + a);
-          else ptx::mbar_arrive_cluster(tempty + a, 0);
+          if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
+          else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
         }
         if (s * 64 >= cols_left || (p.debug & 64)) continue;
         uint32_t pk[32];
+        switch (p.activation) {
+          case kActRelu: pack_chunk<kActRelu>(v0, v1, pk); break;
+          case kActSilu: pack_chunk<kActSilu>(v0, v1, pk); break;
+          case kActGeluTanh: pack_chunk<kActGeluTanh>(v0, v1, pk); break;
+          case kActTanh: pack_chunk<kActTanh>(v0, v1, pk); break;
+          default: pack_chunk<kActIdentity>(v0, v1, pk); break;
+        }
+        // Coalesce through a per-warp smem transpose: each lane parks its
+        // row's 128 B (XOR-swizzled 16 B granules, conflict-free), then each
+        // store instruction writes 4 whole 128 B lines (8 lanes per row).
+        // Only this warp touches its staging rows: __syncwarp suffices.
+        uint8_t* stg = epi_smem + ((s & 1) * 4 + ew) * kSmemEpiWarp;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16(activate(__uint_as_float(v0[2 * i]), p.activation),
-                            activate(__uint_as_float(v0[2 * i + 1]), p.activation));
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        __syncwarp();
+        const int gsub = lane & 7, rsub = lane >> 3;
+        __nv_bfloat16* obase = p.out + static_cast<long long>(row0 + ew * 32) * p.out_ld + w.nb * kBlockN + s * 64;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[16 + i] = pack_bf16(activate(__uint_as_float(v1[2 * i]), p.activation),
-                                 activate(__uint_as_float(v1[2 * i + 1]), p.activation));
-        // direct stores from registers: no smem staging and no TMA store
-        // queued behind the producer's in-flight loads
-        // full 32-byte sectors per store (partial-sector writes cost ~30%)
-        char* dst = reinterpret_cast<char*>(orow + s * 64);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          ptx::st_v8_cs(dst + 32 * c, make_uint4(pk[8 * c], pk[8 * c + 1], pk[8 * c + 2], pk[8 * c + 3]),
-                     make_uint4(pk[8 * c + 4], pk[8 * c + 5], pk[8 * c + 6], pk[8 * c + 7]));
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + rsub;
+          const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 128 + ((gsub ^ (r & 7)) * 16));
+          ptx::st_v4_cs(obase + static_cast<long long>(r) * p.out_ld + gsub * 8, v);
+        }
+        __syncwarp();
       }
       if (p.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
@@ -274,6 +340,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           ptx::red_release_gpu_add(p.nb_done + w.nb, 1u);
         }
       }
+      if (threadIdx.x == kEpiThread0) tl_record(p, kRoleEpilogue, it, u, t_e, ptx::globaltimer());
     }
   }
 

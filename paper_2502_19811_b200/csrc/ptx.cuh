@@ -324,6 +324,10 @@ __device__ __forceinline__ void st_v8(void* p, uint4 lo, uint4 hi) {
   const uint64_t c = (static_cast<uint64_t>(hi.y) << 32) | hi.x, d = (static_cast<uint64_t>(hi.w) << 32) | hi.z;
   asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" :: "l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
+__device__ __forceinline__ void st_v4_cs(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
