@@ -17,6 +17,8 @@ want = {
     "l2_to_sm_bytes": "l1tex__m_xbar2l1tex_read_bytes.sum",
     "sm_clock_hz": "smsp__cycles_elapsed.avg.per_second",
     "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+    "registers": "launch__registers_per_thread",
 }
 units = rows[1]
 res = {}
@@ -31,7 +33,8 @@ for i, r in enumerate(rows[2:]):
         v = float(v.replace(",", ""))
         unit = u.get(m, "")
         scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "usecond": 1e3, "msecond": 1e6,
-                 "nsecond": 1, "Ghz": 1e9, "Mhz": 1e6, "hz": 1}.get(unit, 1)
+                 "nsecond": 1, "us": 1e3, "ms": 1e6, "ns": 1, "Ghz": 1e9, "Mhz": 1e6, "hz": 1,
+                 "GHz": 1e9, "MHz": 1e6}.get(unit, 1)
         rec[k] = v * scale
     if "dram_read" in rec:
         rec["dram_bytes"] = rec["dram_read"] + rec.get("dram_write", 0)
