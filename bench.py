@@ -279,7 +279,7 @@ def run_ours(args):
         n_prof = max(3, min(args.steps, 10))
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_prof)]
         for i in range(n_prof):
-            ctx.index_build(ex, M)
+            ctx.index_build(ex, M, flags=2 if (world > 1 or knobs.n_comm1 > 0) else 0)
             if world > 1:
                 ctx.signal_tokens_ready()
             ev[i][0].record(stream)

@@ -102,6 +102,12 @@ void* comet_routing_buffer(comet_ctx* ctx);
  * Bumps the context epoch (one forward = one epoch). */
 int comet_index_build(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_rows, int tile_cols,
                       void* stream);
+/* Same, choosing what is emitted besides the kernels' work tables:
+ * flags bit0 = reference tile lists (tiles0/tiles1/chunks), bit1 = combine
+ * token list (needed by comm-CTA combine).  comet_index_build = flags 3;
+ * comet_forward builds only what its kernels consume. */
+int comet_index_build_ex(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_rows, int tile_cols,
+                         int flags, void* stream);
 /* Sizes of the index arrays after a build (synchronises the stream). */
 int comet_index_sizes(comet_ctx* ctx, int32_t meta_out[16], void* stream);
 /* Copy the index to host arrays (synchronises the stream). */

@@ -29,7 +29,7 @@ META = {"rows": 0, "rows_pad": 1, "tiles0": 2, "pairs": 3, "pull": 4, "tiles1": 
 EXPORTS = (
     "comet_last_error", "comet_version", "comet_ctx_create", "comet_ctx_destroy",
     "comet_symm_export", "comet_symm_import", "comet_link_local", "comet_token_buffer",
-    "comet_routing_buffer", "comet_index_build", "comet_index_sizes", "comet_index_download",
+    "comet_routing_buffer", "comet_index_build", "comet_index_build_ex", "comet_index_sizes", "comet_index_download",
     "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
     "comet_timeline_enable", "comet_timeline_dump",
@@ -87,6 +87,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_yrows_buffer": ([vp], vp),
         "comet_hidden_rows_cap": ([vp], c.c_int32),
         "comet_index_build": ([vp, vp, i32, i32, i32, vp], i32),
+        "comet_index_build_ex": ([vp, vp, i32, i32, i32, i32, vp], i32),
         "comet_index_sizes": ([vp, _P32, vp], i32),
         "comet_index_download": ([vp, c.POINTER(CometIndexHost), vp], i32),
         "comet_signal_tokens_ready": ([vp, vp], i32),
@@ -211,11 +212,12 @@ class Context:
         return s.cuda_stream
 
     def index_build(self, experts_dev, M: int, tile_rows: int = 128, tile_cols: Optional[int] = None,
-                    stream=None) -> None:
+                    stream=None, flags: int = 3) -> None:
+        """flags: bit0 reference tile lists, bit1 combine token list."""
         if tile_cols is None:  # reference default_tile_cols (resolver.py:35-39)
             tile_cols = 128 if self.N >= 512 else max(1, self.N // 4)
-        check(self.lib.comet_index_build(self.handle, ctypes.c_void_p(experts_dev.data_ptr()), M,
-                                         tile_rows, tile_cols, ctypes.c_void_p(self._stream(stream))))
+        check(self.lib.comet_index_build_ex(self.handle, ctypes.c_void_p(experts_dev.data_ptr()), M,
+                                            tile_rows, tile_cols, flags, ctypes.c_void_p(self._stream(stream))))
 
     def index_meta(self, stream=None) -> np.ndarray:
         meta = (ctypes.c_int32 * 16)()

@@ -184,7 +184,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
   if (c.K % c.tp) return fail(COMET_EINVAL, "K=%d is not divisible by tp=%d", c.K, c.tp);
   if (c.E > 1024) return fail(COMET_EINVAL, "E=%d > 1024 unsupported", c.E);
   if (c.topk < 1 || c.topk > c.E) return fail(COMET_EINVAL, "bad topk %d", c.topk);
-  if (c.m_cap < 1) return fail(COMET_EINVAL, "m_cap must be >= 1");
+  if (c.m_cap < 1 || c.m_cap > 65536) return fail(COMET_EINVAL, "m_cap must be in [1, 65536]");
 
   comet_ctx* x = new comet_ctx();
   x->cfg = c;
@@ -408,7 +408,15 @@ static int ensure_tiles(comet_ctx* x, int tile_rows, int tile_cols) {
   return COMET_OK;
 }
 
+int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile_rows, int tile_cols, int flags,
+                         void* stream);
+
 int comet_index_build(comet_ctx* x, const int32_t* d_experts, int M, int tile_rows, int tile_cols, void* stream) {
+  return comet_index_build_ex(x, d_experts, M, tile_rows, tile_cols, kIndexRefLists | kIndexCombineList, stream);
+}
+
+int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile_rows, int tile_cols, int flags,
+                         void* stream) {
   const auto& c = x->cfg;
   if (M < 0 || M > c.m_cap) return fail(COMET_EINVAL, "M=%d outside [0, m_cap=%d]", M, c.m_cap);
   if (tile_rows < 1) return fail(COMET_EINVAL, "tile_rows must be >= 1, got %d", tile_rows);
@@ -432,11 +440,13 @@ int comet_index_build(comet_ctx* x, const int32_t* d_experts, int M, int tile_ro
   ix.tile_rows = tile_rows;
   ix.tile_cols = tile_cols;
   ix.n_embed = c.N;
+  ix.flags = flags;
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(index_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIndexSmem));
     attr_set = true;
   }
+  CK(cudaMemsetAsync(x->ix.transfer, 0, sizeof(int32_t) * c.world * c.world, static_cast<cudaStream_t>(stream)));
   index_build_kernel<<<x->E_r + 1, kIndexThreads, kIndexSmem, static_cast<cudaStream_t>(stream)>>>(ix);
   CK(cudaGetLastError());
   x->ix.experts = d_experts;  // the layer1 finish kernel reads the global routing
@@ -683,7 +693,10 @@ int comet_combine_finish(comet_ctx* x, void* y_local, void* stream) {
 int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t, const void* w1t,
                   const float* combine_w, void* y_local, int activation, int n_comm0, int n_comm1, int group0,
                   int wave1, void* stream) {
-  if (int rc = comet_index_build(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), stream))
+  // hot path: no reference-format tile lists; combine list only for comm-CTA combine
+  const int flags = (x->cfg.world > 1 || n_comm1 > 0) ? kIndexCombineList : 0;
+  if (int rc = comet_index_build_ex(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), flags,
+                                    stream))
     return rc;
   if (x->cfg.world > 1)
     if (int rc = comet_signal_tokens_ready(x, stream)) return rc;

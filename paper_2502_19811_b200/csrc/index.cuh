@@ -25,12 +25,17 @@ enum MetaSlot : int {
   kMetaSlots = 16
 };
 
+// IndexDev::flags: what the last CTA emits besides the pair tables.
+constexpr int kIndexRefLists = 1;      // reference tiles0 / tiles1 / chunks (resolver API)
+constexpr int kIndexCombineList = 2;   // combine token list (comm-CTA combine)
+
 struct IndexDev {
   // inputs
   const int32_t* experts;   // [M, topk] row-major, ascending per token
   int M, E, topk, tp, ep, rank, world;
   int e_lo, E_r;            // hosted experts [e_lo, e_lo + E_r)
   int tile_rows, tile_cols, n_embed;
+  int flags;
 
   // outputs (device)
   int32_t* counts;      // [E]

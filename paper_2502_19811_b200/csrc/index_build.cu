@@ -71,6 +71,12 @@ __device__ __forceinline__ void warp_add(int* base, int idx, bool active) {
   if ((threadIdx.x & 31) == leader) atomicAdd(base + idx, __popc(peers));
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ int slot_of(const int32_t* row, int topk, int e) {
   for (int s = 0; s < topk; ++s)
     if (row[s] == e) return s;
@@ -94,13 +100,24 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
 
   const int tid = threadIdx.x;
   const int M = ix.M, K = ix.topk, W = ix.world, E = ix.E, Er = ix.E_r;
+  const unsigned long long t_enter = globaltimer_ns();
 
   // -------- phase 0 (every CTA): global histogram + hosted offsets --------
   for (int e = tid; e < E; e += kThreads) s_cnt[e] = 0;
   __syncthreads();
-  for (int i0 = 0; i0 < M * K; i0 += kThreads) {
-    const int i = i0 + tid;
-    warp_add(s_cnt, i < M * K ? ix.experts[i] : 0, i < M * K);
+  {
+    // batched coalesced loads (8 in flight per thread), then aggregated adds
+    constexpr int kB = 8;
+    for (int i0 = 0; i0 < M * K; i0 += kThreads * kB) {
+      int v[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int i = i0 + b * kThreads + tid;
+        v[b] = i < M * K ? __ldg(ix.experts + i) : -1;
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) warp_add(s_cnt, max(v[b], 0), v[b] >= 0);
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -120,32 +137,49 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   const int start = token_start_of(ix.rank, M, W);
   const int n_own = token_stop_of(ix.rank, M, W) - start;
 
+  const unsigned long long t_hist = globaltimer_ns();
   if (blockIdx.x < Er) {
     // -------- per-expert layout: rotated-token stream compaction --------
+    // Thread t owns the contiguous rotated positions [t*per, (t+1)*per):
+    // one batch of independent loads, one block scan for the thread offsets.
     const int j = blockIdx.x, e = ix.e_lo + j;
     const int base_row = s_off[j], base_pad = s_pad[j];
+    const int per = (M + kThreads - 1) / kThreads;
+    constexpr int kMaxPer = 64;  // tokens per thread (host guarantees M <= 64K)
     int running = 0, n_loc = 0;
-    for (int c0 = 0; c0 < M; c0 += kThreads) {
-      const int i = c0 + tid;
-      int t = -1, s = -1;
-      if (i < M) {
-        t = start + i;
+    {
+      const int pass0 = 0;
+      const int cnt_pass = per;
+      uint64_t hit = 0;  // bit q: rotated position tid*per+q routes to e (per <= 64)
+      int mine_loc = 0;
+#pragma unroll 8
+      for (int q = 0; q < cnt_pass; ++q) {  // predicated (no early exit): loads batch up
+        const int i = tid * per + pass0 + q;
+        int t = start + i;
         if (t >= M) t -= M;
-        s = slot_of(ix.experts + static_cast<long long>(t) * K, K, e);
+        const bool f = i < M && slot_of(ix.experts + static_cast<long long>(min(t, M - 1)) * K, K, e) >= 0;
+        hit |= static_cast<uint64_t>(f) << q;
+        mine_loc += (f && i < n_own);
       }
-      const int f = s >= 0 ? 1 : 0;
       int tot;
-      const int pos = running + block_scan(f, s_ws, &tot);
-      if (f) {
+      int pos = running + block_scan(__popcll(hit), s_ws, &tot);
+      while (hit) {
+        const int q = __ffsll(hit) - 1;
+        hit &= hit - 1;
+        const int i = tid * per + pass0 + q;
+        int t = start + i;
+        if (t >= M) t -= M;
+        const int sl = slot_of(ix.experts + static_cast<long long>(t) * K, K, e);
         if (base_row + pos < ix.cap_rows) {
           ix.row_token[base_row + pos] = t;
           ix.row_src[base_row + pos] = src_rank_of(t, M, W);
         }
         if (base_pad + pos < ix.cap_rows_pad) ix.gather_row[base_pad + pos] = t;
-        ix.tok_pos[static_cast<long long>(t) * K + s] = base_pad + pos;
+        ix.tok_pos[static_cast<long long>(t) * K + sl] = base_pad + pos;
+        ++pos;
       }
-      if (i < n_own) n_loc += f;
       running += tot;
+      n_loc += mine_loc;
     }
     // local rows are exactly the rotated prefix [0, n_own)
     int tot;
@@ -153,29 +187,39 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     if (tid == 0) ix.n_local[j] = tot;
     for (int r = base_pad + running + tid; r < s_pad[j + 1]; r += kThreads)
       if (r < ix.cap_rows_pad) ix.gather_row[r] = -1;
-  } else {
-    // -------- bookkeeping CTA: counts, transfer matrix, foreign slots --------
+  }
+  {
+    // -------- bookkeeping, split over every CTA (contiguous token slices):
+    // transfer matrix partials (routing.py:106-117) and the non-hosted slots
     int* s_tr = reinterpret_cast<int*>(sh_keys);  // W*W <= 4096 ints (host-checked)
-    for (int e = tid; e < E; e += kThreads) ix.counts[e] = s_cnt[e];
+    if (blockIdx.x == gridDim.x - 1)
+      for (int e = tid; e < E; e += kThreads) ix.counts[e] = s_cnt[e];
     for (int i = tid; i < W * W; i += kThreads) s_tr[i] = 0;
     __syncthreads();
     const int per_group = E / ix.ep;
-    for (int i0 = 0; i0 < M * K; i0 += kThreads) {
-      const int i = i0 + tid;
-      const bool ok = i < M * K;
-      const int t = ok ? i / K : 0, e = ok ? ix.experts[i] : 0;
-      const int src = src_rank_of(t, M, W);
-      const int g = e / per_group;
-      for (int d = 0; d < ix.tp; ++d) warp_add(s_tr, src * W + g * ix.tp + d, ok);
-      if (ok && (e < ix.e_lo || e >= ix.e_lo + Er)) ix.tok_pos[i] = -1;
+    const int t_lo = static_cast<int>(static_cast<long long>(M) * blockIdx.x / gridDim.x);
+    const int t_hi = static_cast<int>(static_cast<long long>(M) * (blockIdx.x + 1) / gridDim.x);
+    for (int t0 = t_lo; t0 < t_hi; t0 += kThreads) {
+      const int t = t0 + tid;
+      const bool ok = t < t_hi;
+      const int src = src_rank_of(ok ? t : t_lo, M, W);
+      for (int sl = 0; sl < K; ++sl) {
+        const int e = ok ? __ldg(ix.experts + static_cast<long long>(t) * K + sl) : 0;
+        const int g = e / per_group;
+        for (int d = 0; d < ix.tp; ++d) warp_add(s_tr, src * W + g * ix.tp + d, ok);
+        if (ok && (e < ix.e_lo || e >= ix.e_lo + Er)) ix.tok_pos[static_cast<long long>(t) * K + sl] = -1;
+      }
     }
-    for (int i = tid; i < ix.n_zero_words; i += kThreads) ix.zero_words[i] = 0u;
+    for (int i = tid; i < ix.n_zero_words; i += kThreads)
+      if (blockIdx.x == 0) ix.zero_words[i] = 0u;
     __syncthreads();
-    for (int i = tid; i < W * W; i += kThreads) ix.transfer[i] = s_tr[i];
+    for (int i = tid; i < W * W; i += kThreads)
+      if (s_tr[i]) atomicAdd(ix.transfer + i, s_tr[i]);  // zeroed by the host before launch
   }
 
   // -------- grid completion: the last CTA builds the schedules --------
   __syncthreads();
+  const unsigned long long t_phase1 = globaltimer_ns();
   if (tid == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(ix.done, 1u);
@@ -228,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   const bool ovf = T0 > ix.cap_tiles0 || P > ix.cap_pairs || s_pad[Er] > ix.cap_rows_pad ||
                    s_off[Er] > ix.cap_rows;
 
+  const unsigned long long t_p2a = globaltimer_ns();
   // ---- layer0 tiles sorted by (n_deps, expert, row_start) ----
   auto tile_of = [&](int idx, int& j, int& rs, int& re, int& nd) {
     int lo = 0, hi = Er - 1;  // expert with s_t0[j] <= idx < s_t0[j+1]
@@ -243,7 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     nd = (re - rs) - max(0, loc_end - rs);
   };
   const bool keys_in_smem = T0 <= kSortSmemKeys;
-  if (!ovf) {
+  const bool emit_lists = (ix.flags & kIndexRefLists) != 0;
+  if (!ovf && emit_lists) {
     if (keys_in_smem) {
       for (int i = tid; i < T0; i += kThreads) {
         int j, rs, re, nd;
@@ -273,26 +319,44 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     }
   }
   __syncthreads();
+  const unsigned long long t_p2b = globaltimer_ns();
 
   // ---- layer1 reference tiles: column block outer, (expert,row) inner ----
   const int TC = ix.tile_cols, NE = ix.n_embed;
   const int C = (NE + TC - 1) / TC;
   const long long T1 = static_cast<long long>(C) * T0;
-  const bool ovf1 = T1 > ix.cap_tiles1;
-  if (!ovf && !ovf1) {
+  const bool ovf1 = emit_lists && T1 > ix.cap_tiles1;
+  int4* s_tile = reinterpret_cast<int4*>(sh_keys);  // per-tile (expert, rs, re, nd) cache
+  const bool tiles_in_smem = T0 <= kSortSmemKeys / 2;
+  if (!ovf && !ovf1 && emit_lists) {
+    if (tiles_in_smem) {
+      for (int q = tid; q < T0; q += kThreads) {
+        int j, rs, re, nd;
+        tile_of(q, j, rs, re, nd);
+        s_tile[q] = make_int4(ix.e_lo + j, rs, re, nd);
+      }
+      __syncthreads();
+    }
     for (long long i = tid; i < T1; i += kThreads) {
       const int c = static_cast<int>(i / T0), q = static_cast<int>(i % T0);
-      int j, rs, re, nd;
-      tile_of(q, j, rs, re, nd);
+      int4 tq;
+      if (tiles_in_smem) {
+        tq = s_tile[q];
+      } else {
+        int j, rs, re, nd;
+        tile_of(q, j, rs, re, nd);
+        tq = make_int4(ix.e_lo + j, rs, re, nd);
+      }
       int* o = ix.tiles1 + i * 6;
-      o[0] = ix.e_lo + j; o[1] = rs; o[2] = re;
-      o[3] = c * TC; o[4] = min(c * TC + TC, NE); o[5] = nd;
+      o[0] = tq.x; o[1] = tq.y; o[2] = tq.z;
+      o[3] = c * TC; o[4] = min(c * TC + TC, NE); o[5] = tq.w;
     }
     for (int c = tid; c < C; c += kThreads) {
       int* o = ix.chunks + c * 4;
       o[0] = c * TC; o[1] = min(c * TC + TC, NE); o[2] = c * T0; o[3] = T0;
     }
   }
+  __syncthreads();
 
   // ---- 2-CTA pair tables: natural order (layer1) and claim order (layer0) ----
   // A pair's claim key is the key of its last 128-row half, i.e. its position
@@ -313,18 +377,33 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     const int nd = (last_re - last_rs) - max(0, min(last_re, s_nloc[j]) - last_rs);
     key = tile_key(nd, ix.e_lo + j, last_rs);
   };
+  const unsigned long long t_p2c = globaltimer_ns();
+  long long* s_pkey = sh_keys;  // P keys (P <= kSortSmemKeys, else recomputed)
+  const bool pkeys_in_smem = P <= kSortSmemKeys;
   if (!ovf) {
+    if (pkeys_in_smem) {
+      for (int i = tid; i < P; i += kThreads) {
+        int j, prow, valid;
+        long long key;
+        pair_of(i, j, prow, valid, key);
+        s_pkey[i] = key;
+      }
+      __syncthreads();
+    }
     for (int i = tid; i < P; i += kThreads) {
       int j, prow, valid;
       long long key;
       pair_of(i, j, prow, valid, key);
       int* o = ix.pairs1 + i * 4;
-      o[0] = j; o[1] = prow; o[2] = valid; o[3] = 0;
       int rank = 0;
       for (int q = 0; q < P; ++q) {
-        int jq, pq, vq;
         long long kq;
-        pair_of(q, jq, pq, vq, kq);
+        if (pkeys_in_smem) {
+          kq = s_pkey[q];
+        } else {
+          int jq, pq, vq;
+          pair_of(q, jq, pq, vq, kq);
+        }
         rank += kq < key;
       }
       ix.pair_key[i] = rank;
@@ -332,9 +411,9 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       const int r0 = prow - s_pad[j];
       const int remote_mask = (min(r0 + kTileRows, s_cnt[ix.e_lo + j]) > s_nloc[j] ? 1 : 0) |
                               (valid > kTileRows && r0 + valid > s_nloc[j] ? 2 : 0);
+      o[0] = j; o[1] = prow; o[2] = valid; o[3] = remote_mask;
       int* o0 = ix.pairs0 + rank * 4;
       o0[0] = j; o0[1] = prow; o0[2] = valid; o0[3] = remote_mask;
-      o[3] = remote_mask;
     }
   }
   __syncthreads();
@@ -343,26 +422,43 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   if (tid == 0) s_misc[2] = 0;  // pull list retired: remote rows are pulled per tile (comm.cuh)
   __syncthreads();
 
+  const unsigned long long t_p2d = globaltimer_ns();
   // ---- combine token list: tokens with >=1 hosted expert, ascending ----
-  {
-    int running = 0;
-    for (int c0 = 0; c0 < M; c0 += kThreads) {
-      const int t = c0 + tid;
+  if (ix.flags & kIndexCombineList) {
+    const int per = (M + kThreads - 1) / kThreads;
+    uint64_t hits = 0;  // bit q: token tid*per+q has a hosted expert (per <= 64)
+#pragma unroll 8
+    for (int q = 0; q < per; ++q) {
+      const int t = tid * per + q;
       int f = 0;
       if (t < M) {
         const int32_t* row = ix.experts + static_cast<long long>(t) * K;
-        for (int s = 0; s < K; ++s) f |= (row[s] >= ix.e_lo && row[s] < ix.e_lo + Er);
+        for (int s2 = 0; s2 < K; ++s2) {
+          const int ev = __ldg(row + s2);
+          f |= (ev >= ix.e_lo && ev < ix.e_lo + Er);
+        }
       }
-      int tot;
-      const int pos = running + block_scan(f, s_ws, &tot);
-      if (f) ix.combine_tok[pos] = t;
-      running += tot;
+      hits |= static_cast<uint64_t>(f) << q;
     }
-    if (tid == 0) s_misc[3] = running;
+    int tot;
+    int pos = block_scan(__popcll(hits), s_ws, &tot);
+    for (int q = 0; q < per; ++q)
+      if ((hits >> q) & 1) ix.combine_tok[pos++] = tid * per + q;
+    if (tid == 0) s_misc[3] = tot;
+  } else if (tid == 0) {
+    s_misc[3] = 0;
   }
   __syncthreads();
 
   if (tid == 0) {
+    const unsigned long long t_end = globaltimer_ns();
+    ix.meta[8] = static_cast<int>(t_hist - t_enter);
+    ix.meta[9] = static_cast<int>(t_phase1 - t_enter);
+    ix.meta[10] = static_cast<int>(t_end - t_enter);
+    ix.meta[11] = static_cast<int>(t_p2a - t_enter);
+    ix.meta[12] = static_cast<int>(t_p2b - t_enter);
+    ix.meta[13] = static_cast<int>(t_p2c - t_enter);
+    ix.meta[14] = static_cast<int>(t_p2d - t_enter);
     ix.meta[kMetaRows] = s_off[Er];
     ix.meta[kMetaRowsPad] = Rpad;
     ix.meta[kMetaTiles0] = T0;

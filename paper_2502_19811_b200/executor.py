@@ -314,7 +314,9 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
     layer1 -> remote combine)."""
     world = layers[0].parallel.world_size
     for layer in layers:
-        layer.ctx.index_build(ex, M, stream=stream)
+        # hot path: the kernels' tables only (+ the combine list for comm-CTA combine)
+        flags = 2 if (world > 1 or layer.knobs.n_comm1 > 0) else 0
+        layer.ctx.index_build(ex, M, stream=stream, flags=flags)
     if world > 1:
         for layer in layers:
             layer.ctx.signal_tokens_ready(stream=stream)
