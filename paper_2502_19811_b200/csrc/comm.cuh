@@ -32,8 +32,18 @@ struct CommSmem {
   JobDesc desc[kMaxSlots];
   int pub_tile[64];
   int pub_job[64];
+  unsigned long long pub_t0[64];
   const __nv_bfloat16* xs_peer[kMaxWorld];
 };
+
+// Timeline record of a communication task (same buffer/format as the compute
+// roles, moe_layers.cu tl_record): role kRoleComm, task = tile or n-block id.
+__device__ __forceinline__ void comm_record(const LayerArgs& p, int idx, int task, uint64_t t0, uint64_t t1) {
+  if (p.timeline == nullptr || idx >= p.timeline_cap) return;
+  unsigned long long* r = p.timeline + ((static_cast<long long>(blockIdx.x) * kRoles + kRoleComm) * p.timeline_cap + idx) * 2;
+  r[0] = t0;
+  r[1] = (t1 - t0) | (static_cast<unsigned long long>(task + 1) << 40);
+}
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -116,17 +126,22 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
     }
   } else if (warp == 1 && lane == 0) {
     // ---- storer: slot -> xg row; publish tiles once their writes landed ----
-    int k = 0, head = 0, tail = 0;
+    int k = 0, head = 0, tail = 0, n_rec = 0;
     auto publish_upto = [&](int done_job) {
       while (head != tail && cs->pub_job[head & 63] <= done_job) {
         ptx::fence_async_global();
+        // end stamp taken before the release: a consumer that observes the
+        // flag always stamps a later time (measured dependency audit)
+        const unsigned long long t_pub = ptx::globaltimer();
         ptx::st_release_gpu(p.xg_ready + cs->pub_tile[head & 63], p.epoch);
+        comm_record(p, n_rec++, cs->pub_tile[head & 63], cs->pub_t0[head & 63], t_pub);
         ++head;
       }
     };
     for (int q = cid; q < n_tiles; q += n_comm) {
       int padrow0, nr;
       if (!remote_rows(p, q, padrow0, nr)) continue;
+      const unsigned long long t_tile = ptx::globaltimer();
       for (int r = 0; r < nr; ++r, ++k) {
         const int slot = k % n_slots;
         ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
@@ -141,6 +156,7 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
       }
       cs->pub_tile[tail & 63] = q;
       cs->pub_job[tail & 63] = k - 1;
+      cs->pub_t0[tail & 63] = t_tile;
       ++tail;
       if (tail - head >= 60) {
         ptx::bulk_wait<0>();
@@ -183,6 +199,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
       if (lane == 0)
         while (ptx::ld_acquire_gpu(p.nb_done + nb) < target) __nanosleep(128);
       __syncwarp();
+      const unsigned long long t_nb = ptx::globaltimer();
       const uint32_t seg = min(kSeg, static_cast<uint32_t>(N - nb * kBlockN) * 2u);
       for (int j0 = 0; j0 < jobs; j0 += kBatch) {
         const int j = j0 + lane;
@@ -216,6 +233,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
         k += min(kBatch, jobs - j0);
         __syncwarp();
       }
+      if (lane == 0) comm_record(p, nb, nb, t_nb, ptx::globaltimer());
     }
     return;
   }

@@ -191,7 +191,6 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     uint32_t phase = 0;
     int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const uint64_t t_start = ptx::globaltimer();
       const Unit w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
@@ -203,6 +202,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         ptx::fence_async_global();
       }
       __syncwarp();
+      const uint64_t t_start = ptx::globaltimer();  // load interval starts once its A rows are ready
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         wait(empty + stage, phase ^ 1);
         if (lane == 0 && (p.debug & 16)) {

@@ -1,0 +1,55 @@
+"""Per-rank kernel times of an EP=W layer emulated on one GPU (all ranks'
+heaps on this device; NVLink traffic becomes local HBM traffic)."""
+import os, sys, statistics
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2502_19811_b200 import LayerKnobs, ModelConfig, ParallelSpec, WorkloadSpec, build_routing
+from paper_2502_19811_b200.executor import MoELayer, RankWeights, _lib
+
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+nc0 = int(os.environ.get("NC0", 2)); nc1 = int(os.environ.get("NC1", 4))
+E, topk, N, K, M = 8, 2, 4096, 14336, 8192
+model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
+par = ParallelSpec(1, W)
+r = build_routing(model, par, WorkloadSpec(M=M, seed=0))
+g = torch.Generator(device="cuda").manual_seed(0)
+layers = []
+for rank in range(W):
+    e_per = E // W
+    w0t = (torch.randn(e_per, K, N, device="cuda", generator=g) / 64).to(torch.bfloat16)
+    w1t = (torch.randn(e_per, N, K, device="cuda", generator=g) / 64).to(torch.bfloat16)
+    layers.append(MoELayer(model, par, rank, M, RankWeights(w0t, w1t), knobs=LayerKnobs(n_comm0=nc0, n_comm1=nc1)))
+_lib.Context.link_local([l.ctx for l in layers])
+x = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+ex = torch.from_numpy(r.as_array().copy()).cuda()
+ys = []
+for l in layers:
+    lo, hi = l.token_range(M)
+    l.place_tokens(x[lo:hi], M)
+    ys.append(torch.empty(hi - lo, N, dtype=torch.bfloat16, device="cuda"))
+ev = lambda: torch.cuda.Event(enable_timing=True)
+res = {k: [] for k in ("index", "layer0", "layer1", "finish")}
+for it in range(6):
+    for l in layers:
+        l.ctx.index_build(ex, M, flags=2)
+    for l in layers:
+        l.ctx.signal_tokens_ready()
+    t = []
+    for l in layers:
+        a, b = ev(), ev(); a.record(); l.ctx.layer0(l.weights.w0t, 0, nc0, 4); b.record(); t.append((a, b))
+    t1 = []
+    for l, y in zip(layers, ys):
+        a, b = ev(), ev(); a.record(); l.ctx.layer1(l.weights.w1t, None, y, nc1, 4); b.record(); t1.append((a, b))
+    t2 = []
+    for l, y in zip(layers, ys):
+        a, b = ev(), ev(); a.record(); l.ctx.combine_finish(y); b.record(); t2.append((a, b))
+    torch.cuda.synchronize()
+    if it >= 2:
+        res["layer0"].append(max(a.elapsed_time(b) for a, b in t))
+        res["layer1"].append(max(a.elapsed_time(b) for a, b in t1))
+        res["finish"].append(max(a.elapsed_time(b) for a, b in t2))
+rows = layers[0].ctx.index_meta()[0]
+fl = 2.0 * rows * N * K / W * W  # per rank (tp=1): 2*rows*N*K
+print(f"EP={W} rank rows={rows}: layer0 {statistics.median(res['layer0']):.3f} ms, layer1 {statistics.median(res['layer1']):.3f} ms, "
+      f"finish {statistics.median(res['finish']):.3f} ms (max over ranks); per-layer TF/s "
+      f"{2.0*rows*N*K/statistics.median(res['layer0'])/1e9:.0f} / {2.0*rows*N*K/statistics.median(res['layer1'])/1e9:.0f}")
