@@ -244,7 +244,7 @@ def run_ours(args):
     routing = build_routing(model, par, WorkloadSpec(M=args.M, seed=0, std=args.std))
     M = args.M
     dev = torch.device("cuda", local)
-    knobs = LayerKnobs(n_comm0=args.n_comm0, n_comm1=args.n_comm1 if world == 1 else max(2, args.n_comm1),
+    knobs = LayerKnobs(n_comm0=args.n_comm0, n_comm1=args.n_comm1,
                        group0=args.group0, wave1=args.wave1)
     weights = rank_weights_random(model, par, rank, dev)
     layer = distributed.init_layer(model, par, M, weights, knobs=knobs) if world > 1 else \
@@ -285,7 +285,7 @@ def run_ours(args):
             ev[i][0].record(stream)
             ctx.layer0(layer.weights.w0t, layer.act, knobs.n_comm0 if world > 1 else 0, knobs.group0)
             ev[i][1].record(stream)
-            ctx.layer1(layer.weights.w1t, None, y, knobs.n_comm1, knobs.wave1)
+            ctx.layer1(layer.weights.w1t, None, y, layer.n_comm1(), knobs.wave1)
             ev[i][2].record(stream)
             ctx.combine_finish(y)
             ev[i][3].record(stream)

@@ -132,7 +132,8 @@ struct comet_ctx {
   __nv_bfloat16* yrows = nullptr;
   __nv_bfloat16* xg = nullptr;      // dispatched (expert-sorted) layer0 rows
   uint32_t* xg_ready = nullptr;     // per 128-row tile epoch
-  uint32_t* counters = nullptr;  // nb_done[nb1] | nb_sent[nb1]
+  uint32_t* counters = nullptr;   // nb_done[nb1] | nb_sent[nb1]
+  uint32_t* tile_done = nullptr;  // [Rpad/128 + 1][nb1] fused-combine tile epochs
   int32_t* routing = nullptr;
 
   CUtensorMap tm_xs, tm_H, tm_y, tm_xg;
@@ -224,6 +225,8 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       {&ix.pull_token, (size_t)c.m_cap},
       {&ix.pull_src, (size_t)c.m_cap},
       {&ix.combine_tok, (size_t)c.m_cap},
+      {&ix.row_dst, (size_t)x->cap_rows_pad},
+      {&ix.row_widx, (size_t)x->cap_rows_pad},
       {&ix.meta, (size_t)kMetaSlots},
       {&ix.first_key, (size_t)c.m_cap},
       {&ix.key_slot, (size_t)x->cap_rows_pad},
@@ -249,6 +252,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
 
   // ---- symmetric region ----
   x->mloc_cap = c.m_cap / W + W;
+  ix.mloc_cap = x->mloc_cap;
   const size_t xs_b = align_up((size_t)c.m_cap * c.N * 2, 4096);
   const size_t tr_b = align_up((size_t)c.m_cap * 4, 4096);
   const size_t xr_b = 4096;
@@ -300,6 +304,7 @@ int comet_ctx_destroy(comet_ctx* x) {
   cudaFree(x->yrows);
   cudaFree(x->xg);
   cudaFree(x->xg_ready);
+  cudaFree(x->tile_done);
   cudaFree(x->timeline);
   cudaFree(x->counters);
   cudaFree(x->routing);
@@ -510,6 +515,9 @@ static int ensure_work(comet_ctx* x) {
   CK(cudaMalloc(&x->xg, (size_t)x->cap_rows_pad * c.N * 2));
   CK(cudaMalloc(&x->xg_ready, sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
   CK(cudaMemset(x->xg_ready, 0, sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
+  const size_t td = sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1) * x->nb1;
+  CK(cudaMalloc(&x->tile_done, td));
+  CK(cudaMemset(x->tile_done, 0, td));
   int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
   if (!rc) rc = make_map(&x->tm_xg, x->xg, x->cap_rows_pad, c.N, 128);
   if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
@@ -551,6 +559,8 @@ static LayerArgs base_args(comet_ctx* x) {
   a.pull_src = x->ix.pull_src;
   a.tok_pos = x->ix.tok_pos;
   a.combine_tok = x->ix.combine_tok;
+  a.row_dst = x->ix.row_dst;
+  a.row_widx = x->ix.row_widx;
   const int W = c.world;
   a.xs_local = x->xs;
   a.xs_peer = reinterpret_cast<const __nv_bfloat16* const*>(x->peer_tab);
@@ -622,7 +632,7 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
                  void* stream) {
   const auto& c = x->cfg;
   if (wave < 1) return fail(COMET_EINVAL, "wave must be >= 1");
-  if (c.world > 1 && n_comm < 2) return fail(COMET_EINVAL, "world > 1: layer1 needs n_comm >= 2 (combine CTAs)");
+  if (n_comm < 0) return fail(COMET_EINVAL, "n_comm=%d must be >= 0", n_comm);
   CK(cudaSetDevice(c.device));
   if (int rc = ensure_work(x)) return rc;
   if (int rc = get_weight_map(x, x->w1c, w1t, (uint64_t)x->E_r * c.N, x->k_local)) return rc;
@@ -638,9 +648,19 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   a.out_ld = c.N;
   a.combine_w = combine_w;
   a.y_local = static_cast<__nv_bfloat16*>(y_local);
+  // Fused combine (world > 1 always; world 1 when no combine CTAs are asked
+  // for and COMET_FUSE1=1): the epilogue of each token's last hosted row
+  // folds the earlier rows in and writes / pushes the result, so layer1 runs
+  // without communication CTAs.  Otherwise combine CTAs (n_comm > 0) or the
+  // local combine kernel reduce yrows.  At world 1 the fold's tile waits cost
+  // what the local combine kernel saves (A/B in DESIGN.md), so it is opt-in.
+  const char* f1 = getenv("COMET_FUSE1");
+  a.fuse_combine = c.world > 1 || (n_comm == 0 && f1 != nullptr && atoi(f1) != 0);
+  a.tile_done = x->tile_done;
+  if (c.world > 1) n_comm = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (int rc = launch_layer(x, a, x->tm_H, x->w1c.map, x->tm_y, n_comm, st)) return rc;
-  if (n_comm == 0) {
+  if (n_comm == 0 && !a.fuse_combine) {
     const int t0 = token_start_of(c.rank, x->M, c.world);
     const int n_tok = token_stop_of(c.rank, x->M, c.world) - t0;
     combine_local_kernel<<<x->n_sm * 8, 256, 0, st>>>(x->ix.tok_pos, combine_w, x->yrows,

@@ -45,6 +45,19 @@ __device__ __forceinline__ void comm_record(const LayerArgs& p, int idx, int tas
   r[1] = (t1 - t0) | (static_cast<unsigned long long>(task + 1) << 40);
 }
 
+// Layer1 (world > 1): one contributor finished its rows of column block nb --
+// a compute CTA's 128 epilogue-pushed rows of one unit, or a combine CTA's
+// reduced tokens.  The contributor completing the count (2 per pair unit + one
+// per combine CTA) publishes the block to every peer's combine flags.
+__device__ __forceinline__ void nb_contributed(const LayerArgs& p, int nb, uint32_t target) {
+  ptx::fence_acq_rel_sys();
+  const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.nb_sent + nb, 1u);
+  if (prev + 1u == target) {
+    ptx::fence_acq_rel_sys();
+    for (int d = 0; d < p.world; ++d) ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * p.n_blocks + nb, p.epoch);
+  }
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -280,13 +293,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
       // all reducers of this CTA finished nb -> count the CTA; last CTA signals peers
       __threadfence_system();
       ptx::named_bar_sync(2, kReducers * 32);
-      if (threadIdx.x == 32) {
-        const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.nb_sent + nb, 1u);
-        if (prev == static_cast<uint32_t>(n_comm) - 1) {
-          ptx::fence_acq_rel_sys();
-          for (int d = 0; d < p.world; ++d) ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * NB + nb, p.epoch);
-        }
-      }
+      if (threadIdx.x == 32) nb_contributed(p, nb, target + static_cast<uint32_t>(n_comm));
     }
   }
 }

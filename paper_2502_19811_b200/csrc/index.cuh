@@ -36,6 +36,7 @@ struct IndexDev {
   int e_lo, E_r;            // hosted experts [e_lo, e_lo + E_r)
   int tile_rows, tile_cols, n_embed;
   int flags;
+  int mloc_cap;             // combine slots per sender in the symmetric combine buffer
 
   // outputs (device)
   int32_t* counts;      // [E]
@@ -54,7 +55,10 @@ struct IndexDev {
   int32_t* pairs1;      // [P*4] (e_local, pad_row, valid_rows, 0) expert/row order
   int32_t* pull_token;  // [<=M] remote tokens in first-demand order
   int32_t* pull_src;    // [<=M]
-  int32_t* combine_tok; // [<=M] tokens with a hosted expert, ascending
+  int32_t* combine_tok; // [<=M] tokens with a hosted expert, ascending (combine CTAs)
+  int32_t* row_dst;     // [Rpad] (src_rank << 24 | combine slot) of a padded row holding its
+                        // token's last hosted expert (fused combine), else -1
+  int32_t* row_widx;    // [Rpad] t * topk + slot of the padded row (combine weight index)
   int32_t* meta;        // [kMetaSlots]
   // scratch
   int32_t* first_key;   // [M]  demand key per token (INT_MAX = not needed)

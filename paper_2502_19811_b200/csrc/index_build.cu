@@ -169,7 +169,18 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
         const int i = tid * per + pass0 + q;
         int t = start + i;
         if (t >= M) t -= M;
-        const int sl = slot_of(ix.experts + static_cast<long long>(t) * K, K, e);
+        const int32_t* trow = ix.experts + static_cast<long long>(t) * K;
+        const int sl = slot_of(trow, K, e);
+        if (base_pad + pos < ix.cap_rows_pad) {
+          // the token's last hosted expert (ascending slots) carries the fused
+          // combine: its epilogue folds the earlier hosted rows in
+          bool last = true;
+          for (int s2 = sl + 1; s2 < K; ++s2) last &= !(trow[s2] >= ix.e_lo && trow[s2] < ix.e_lo + Er);
+          const int sr = src_rank_of(t, M, W);
+          const int slot = (W > 1 ? ix.rank * ix.mloc_cap : 0) + t - token_start_of(sr, M, W);
+          ix.row_dst[base_pad + pos] = last ? ((sr << 24) | slot) : -1;
+          ix.row_widx[base_pad + pos] = t * K + sl;
+        }
         if (base_row + pos < ix.cap_rows) {
           ix.row_token[base_row + pos] = t;
           ix.row_src[base_row + pos] = src_rank_of(t, M, W);
@@ -186,7 +197,11 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     block_scan(n_loc, s_ws, &tot);
     if (tid == 0) ix.n_local[j] = tot;
     for (int r = base_pad + running + tid; r < s_pad[j + 1]; r += kThreads)
-      if (r < ix.cap_rows_pad) ix.gather_row[r] = -1;
+      if (r < ix.cap_rows_pad) {
+        ix.gather_row[r] = -1;
+        ix.row_dst[r] = -1;
+        ix.row_widx[r] = 0;
+      }
   }
   {
     // -------- bookkeeping, split over every CTA (contiguous token slices):
@@ -435,10 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
         const int32_t* row = ix.experts + static_cast<long long>(t) * K;
         for (int s2 = 0; s2 < K; ++s2) {
           const int ev = __ldg(row + s2);
-          f |= (ev >= ix.e_lo && ev < ix.e_lo + Er);
+          f += (ev >= ix.e_lo && ev < ix.e_lo + Er);
         }
       }
-      hits |= static_cast<uint64_t>(f) << q;
+      hits |= static_cast<uint64_t>(f > 0) << q;
     }
     int tot;
     int pos = block_scan(__popcll(hits), s_ws, &tot);

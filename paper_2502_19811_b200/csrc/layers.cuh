@@ -42,6 +42,11 @@ struct LayerArgs {
   const int32_t* pull_src;
   const int32_t* tok_pos;     // [M*topk]
   const int32_t* combine_tok;
+  const int32_t* row_dst;     // [Rpad] (src_rank << 24 | combine slot) of last-hosted rows, else -1
+  const int32_t* row_widx;    // [Rpad] t * topk + slot of each padded row
+  int fuse_combine;           // layer1: the epilogue of each token's last hosted row folds the
+                              // earlier rows in and writes y (world 1) / pushes to the source rank
+  uint32_t* tile_done;        // [Rpad/128 * n_blocks] epoch when a 128-row tile's yrows of an n-block landed
   const float* combine_w;     // [M*topk] or null
 
   // buffers

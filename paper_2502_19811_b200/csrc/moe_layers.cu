@@ -129,6 +129,21 @@ __device__ __forceinline__ void pack_chunk(const uint32_t (&v0)[32], const uint3
     pk[16 + i] = pack_bf16(activate<ACT>(__uint_as_float(v1[2 * i])), activate<ACT>(__uint_as_float(v1[2 * i + 1])));
 }
 
+// acc[0..32) += w * 32 bf16 of an earlier expert row (fused combine fold)
+__device__ __forceinline__ void fold_row(uint32_t (&acc)[32], const __nv_bfloat16* src, float w) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src + q * 8);  // written by this kernel: no .nc
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      acc[q * 8 + 2 * j] = __float_as_uint(fmaf(w, f.x, __uint_as_float(acc[q * 8 + 2 * j])));
+      acc[q * 8 + 2 * j + 1] = __float_as_uint(fmaf(w, f.y, __uint_as_float(acc[q * 8 + 2 * j + 1])));
+    }
+  }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -184,6 +199,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
   const int U = P * NB;
   const int pair_id = blockIdx.x >> 1;
   const int n_pairs = p.n_compute >> 1;
+  if (p.layer == 1 && p.world > 1 && P == 0 && gridDim.x == static_cast<unsigned>(p.n_compute) &&
+      blockIdx.x == 0 && threadIdx.x == 0)  // nothing hosted, no combine CTAs: publish empty blocks
+    for (int nb = 0; nb < NB; ++nb)
+      for (int d = 0; d < p.world; ++d) ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * NB + nb, p.epoch);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -282,6 +301,34 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
       const uint64_t t_e = ptx::globaltimer();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
       const int cols_left = p.out_ld - w.nb * kBlockN;  // ragged last n-block (e.g. K/tp = 3200)
+      // Destination of this lane's row: the layer output, or -- fused combine,
+      // the row of its token's last hosted expert -- the token's weighted sum
+      // over its hosted experts (executor.py:102-120), written to y (world 1)
+      // or pushed straight into the source rank's combine slot over NVLink.
+      const int my_row = row0 + ew * 32 + lane;
+      __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN;
+      float scale = 1.f;
+      int fold_t = -1, fold_s = 0;  // token and own slot of a last-hosted row
+      if (p.layer == 1 && p.fuse_combine) {
+        const int rd = p.row_dst[my_row];
+        if (rd >= 0) {
+          __nv_bfloat16* base = p.world > 1 ? p.cb_peer[rd >> 24] : p.y_local;
+          my_dst = base + static_cast<long long>(rd & 0xFFFFFF) * p.n_embed + w.nb * kBlockN;
+          const int widx = p.row_widx[my_row];
+          fold_t = widx / p.topk;
+          fold_s = widx - fold_t * p.topk;
+          if (p.combine_w) scale = p.combine_w[widx];
+          // earlier hosted rows live in pairs claimed before this one (same
+          // n-block, lower unit index): wait for their 128-row tiles
+          for (int s2 = 0; s2 < fold_s; ++s2) {
+            const int pos = p.tok_pos[fold_t * p.topk + s2];
+            if (pos < 0) continue;
+            const uint32_t* f = p.tile_done + static_cast<long long>(pos >> 7) * NB + w.nb;
+            while (!ptx::epoch_reached(ptx::ld_acquire_gpu(f), p.epoch)) __nanosleep(64);
+          }
+        }
+      }
+      const unsigned long long my_addr = reinterpret_cast<unsigned long long>(my_dst);
 #pragma unroll 1
       for (int s = 0; s < static_cast<int>(kBlockN / 64); ++s) {
         const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
@@ -304,6 +351,21 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
         }
         if (s * 64 >= cols_left || (p.debug & 64)) continue;
+        if (p.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v0[i] = __float_as_uint(__uint_as_float(v0[i]) * scale);
+            v1[i] = __float_as_uint(__uint_as_float(v1[i]) * scale);
+          }
+          for (int s2 = 0; s2 < fold_s; ++s2) {
+            const int pos = p.tok_pos[fold_t * p.topk + s2];
+            if (pos < 0) continue;
+            const float ws = p.combine_w ? p.combine_w[fold_t * p.topk + s2] : 1.f;
+            const __nv_bfloat16* src = p.yrows + static_cast<long long>(pos) * p.n_embed + w.nb * kBlockN + s * 64;
+            fold_row(v0, src, ws);
+            fold_row(v1, src + 32, ws);
+          }
+        }
         uint32_t pk[32];
         switch (p.activation) {
           case kActRelu: pack_chunk<kActRelu>(v0, v1, pk); break;
@@ -323,21 +385,26 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         __syncwarp();
         const int gsub = lane & 7, rsub = lane >> 3;
-        __nv_bfloat16* obase = p.out + static_cast<long long>(row0 + ew * 32) * p.out_ld + w.nb * kBlockN + s * 64;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + rsub;
           const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 128 + ((gsub ^ (r & 7)) * 16));
-          ptx::st_v4_cs(obase + static_cast<long long>(r) * p.out_ld + gsub * 8, v);
+          __nv_bfloat16* rp = reinterpret_cast<__nv_bfloat16*>(__shfl_sync(0xffffffffu, my_addr, r));
+          if (p.layer == 1) ptx::st_v4(rp + s * 64 + gsub * 8, v);  // re-read by the fold / combine
+          else ptx::st_v4_cs(rp + s * 64 + gsub * 8, v);
         }
         __syncwarp();
       }
       if (p.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
+        if (p.world > 1) __threadfence_system();  // pushed rows visible to the peer first
         ptx::named_bar_sync(1, 128);
         if (threadIdx.x == kEpiThread0) {
           __threadfence();
           ptx::red_release_gpu_add(p.nb_done + w.nb, 1u);
+          if (p.fuse_combine) ptx::st_release_gpu(p.tile_done + static_cast<long long>(row0 >> 7) * NB + w.nb, p.epoch);
+          if (p.world > 1)
+            comm::nb_contributed(p, w.nb, 2u * static_cast<uint32_t>(P) + (gridDim.x - p.n_compute));
         }
       }
       if (threadIdx.x == kEpiThread0) tl_record(p, kRoleEpilogue, it, u, t_e, ptx::globaltimer());

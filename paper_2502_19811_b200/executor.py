@@ -193,6 +193,18 @@ class MoELayer:
             raise ConfigurationError(f"rank {self.rank} owns {hi - lo} tokens, got {x_local.shape[0]}")
         self._xbuf[lo:hi, :x_local.shape[1]].copy_(x_local, non_blocking=True)
 
+    def n_comm1(self) -> int:
+        """Combine CTAs layer1 launches with.  world > 1: rows of tokens with a
+        single hosted expert are pushed by the epilogue; the combine CTAs reduce
+        tokens with >= 2 hosted experts, so they may be 0 only when no token can
+        have two (one expert per EP group, or top-1)."""
+        k, world = self.knobs, self.parallel.world_size
+        if world == 1:
+            return k.n_comm1
+        if self.model.E // self.parallel.ep == 1 or self.model.topk == 1:
+            return k.n_comm1
+        return max(2, k.n_comm1)
+
     def run(self, experts, M: int, y_local, combine_w=None, stream=None) -> None:
         """Index build + layer0 + layer1 (+ remote combine) on ``stream``;
         tokens must already be in place (``place_tokens``)."""
@@ -200,7 +212,7 @@ class MoELayer:
         world = self.parallel.world_size
         self.ctx.forward(experts, M, self.weights.w0t, self.weights.w1t, combine_w, y_local,
                          activation=self.act, n_comm0=k.n_comm0 if world > 1 else 0,
-                         n_comm1=k.n_comm1 if world == 1 else max(2, k.n_comm1),
+                         n_comm1=self.n_comm1(),
                          group0=k.group0, wave1=k.wave1, stream=stream)
 
     def forward(self, x_local, experts, combine_w=None, M: Optional[int] = None):
@@ -325,7 +337,7 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
         layer.ctx.layer0(layer.weights.w0t, layer.act, k.n_comm0 if world > 1 else 0, k.group0, stream=stream)
     for layer, y in zip(layers, outs):
         k = layer.knobs
-        layer.ctx.layer1(layer.weights.w1t, cw, y, k.n_comm1 if world == 1 else max(2, k.n_comm1), k.wave1,
+        layer.ctx.layer1(layer.weights.w1t, cw, y, layer.n_comm1(), k.wave1,
                          stream=stream)
     if world > 1:
         for layer, y in zip(layers, outs):

@@ -84,8 +84,13 @@ def test_emulated_parallel_layouts_vs_oracle(tp, ep, std):
     assert_close(y, ref, what=f"tp={tp} ep={ep} std={std}")
 
 
-@pytest.mark.parametrize("n_comm1", [0, 2, 6])
-def test_combine_paths_agree(n_comm1):
+@pytest.mark.parametrize("n_comm1", [0, 2, 6, "fused"])
+def test_combine_paths_agree(n_comm1, monkeypatch):
+    """world 1: local combine kernel, combine CTAs, and the epilogue-fused
+    combine (COMET_FUSE1=1: last hosted row folds the earlier ones) agree."""
+    if n_comm1 == "fused":
+        monkeypatch.setenv("COMET_FUSE1", "1")
+        n_comm1 = 0
     model = ModelConfig(L=1, E=8, topk=3, N=512, K=1024)
     routing = build_routing(model, ParallelSpec(), WorkloadSpec(M=777, seed=9, std=0.05))
     w = random_weights(model, seed=1)
@@ -94,6 +99,21 @@ def test_combine_paths_agree(n_comm1):
                      knobs=LayerKnobs(n_comm1=n_comm1)).cpu().numpy()
     ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), np.tanh)
     assert_close(y, ref, what=f"n_comm1={n_comm1}")
+
+
+@pytest.mark.parametrize("ep,std", [(2, 0.0), (4, 0.05)])
+def test_fused_combine_long_fold_chains(ep, std):
+    """Qwen-style top-8: a token's hosted experts form fold chains of up to 7
+    earlier rows in other pairs; the last row's epilogue waits for their tiles
+    and pushes the weighted sum to the source rank."""
+    model = ModelConfig(L=1, E=16, topk=8, N=256, K=512)
+    routing = build_routing(model, ParallelSpec(1, ep), WorkloadSpec(M=700, seed=11, std=std))
+    w = random_weights(model, seed=12)
+    x = np.random.default_rng(13).standard_normal((700, 256))
+    cw = np.random.default_rng(14).random((700, 8))
+    y = run_emulated(x, w, routing, ParallelSpec(1, ep), combine_weights=cw).cpu().numpy()
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), combine_weights=cw)
+    assert_close(y, ref, what=f"top-8 ep={ep}")
 
 
 def test_edge_cases():

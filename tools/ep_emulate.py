@@ -53,3 +53,32 @@ fl = 2.0 * rows * N * K / W * W  # per rank (tp=1): 2*rows*N*K
 print(f"EP={W} rank rows={rows}: layer0 {statistics.median(res['layer0']):.3f} ms, layer1 {statistics.median(res['layer1']):.3f} ms, "
       f"finish {statistics.median(res['finish']):.3f} ms (max over ranks); per-layer TF/s "
       f"{2.0*rows*N*K/statistics.median(res['layer0'])/1e9:.0f} / {2.0*rows*N*K/statistics.median(res['layer1'])/1e9:.0f}")
+
+if os.environ.get("TL"):
+    # one more forward with timelines on rank 0: per-role busy and spans
+    l0 = layers[0]
+    l0.ctx.timeline_enable(256)
+    for l in layers:
+        l.ctx.index_build(ex, M, flags=2)
+    for l in layers:
+        l.ctx.signal_tokens_ready()
+    for l in layers:
+        l.ctx.layer0(l.weights.w0t, 0, nc0, 4)
+    torch.cuda.synchronize()
+    for tag in ("layer0", "layer1"):
+        if tag == "layer1":
+            for l, y in zip(layers, ys):
+                l.ctx.layer1(l.weights.w1t, None, y, nc1, 4)
+            for l, y in zip(layers, ys):
+                l.ctx.combine_finish(y)
+            torch.cuda.synchronize()
+        recs = l0.ctx.timeline_dump()
+        t0 = min(r_[3] for r_ in recs)
+        print(f"== rank0 {tag}: span {(max(r_[4] for r_ in recs) - t0)/1e3:.1f} us")
+        for role in ("load", "mma", "tmem_wait", "epilogue", "comm"):
+            d = [r_ for r_ in recs if r_[1] == role]
+            if d:
+                print(f"   {role:9s} n={len(d):5d} first start +{(min(x[3] for x in d)-t0)/1e3:8.1f}us last end +{(max(x[4] for x in d)-t0)/1e3:8.1f}us mean {statistics.mean(x[4]-x[3] for x in d)/1e3:7.2f}us")
+        if tag == "layer1":
+            for x in sorted([r_ for r_ in recs if r_[1] == "comm"], key=lambda x: x[3])[:40]:
+                print("     comm cta", x[0], "nb", x[2], f"+{(x[3]-t0)/1e3:.1f} .. +{(x[4]-t0)/1e3:.1f}")
