@@ -235,6 +235,7 @@ def run_ours(args):
     rank, world, local = dist_setup(args.gpus)
     from paper_2502_19811_b200 import (LayerKnobs, ModelConfig, MoELayer, ParallelSpec, WorkloadSpec,
                                        build_routing, distributed)
+    from paper_2502_19811_b200.executor import index_flags
     E, topk, N, K, tp = SHAPES[args.shape]
     if world % tp:
         tp = 1
@@ -279,9 +280,7 @@ def run_ours(args):
         n_prof = max(3, min(args.steps, 10))
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_prof)]
         for i in range(n_prof):
-            ctx.index_build(ex, M, flags=2 if (world > 1 or knobs.n_comm1 > 0) else 0)
-            if world > 1:
-                ctx.signal_tokens_ready()
+            ctx.index_build(ex, M, flags=index_flags(world, layer.n_comm1()))
             ev[i][0].record(stream)
             ctx.layer0(layer.weights.w0t, layer.act, knobs.n_comm0 if world > 1 else 0, knobs.group0)
             ev[i][1].record(stream)

@@ -228,8 +228,8 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       {&ix.row_dst, (size_t)x->cap_rows_pad},
       {&ix.row_widx, (size_t)x->cap_rows_pad},
       {&ix.meta, (size_t)kMetaSlots},
-      {&ix.first_key, (size_t)c.m_cap},
-      {&ix.key_slot, (size_t)x->cap_rows_pad},
+      {&ix.chunk_cnt, (size_t)x->E_r * kIndexMaxChunks},
+      {&ix.chunk_loc, (size_t)x->E_r * kIndexMaxChunks},
       {&ix.pair_key, (size_t)x->cap_pairs},
   };
   size_t total = 0;
@@ -245,6 +245,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       b += align_up(p.n * 4, 256);
     }
     ix.done = reinterpret_cast<uint32_t*>(b);
+    ix.gbar = ix.done + 1;
   }
   ix.cap_rows = x->cap_rows;
   ix.cap_rows_pad = x->cap_rows_pad;
@@ -446,13 +447,21 @@ int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile
   ix.tile_cols = tile_cols;
   ix.n_embed = c.N;
   ix.flags = flags;
+  ix.epoch = x->epoch;
+  ix.x_ready_peer = reinterpret_cast<uint32_t* const*>(x->peer_tab + 3 * c.world);
+  ix.tpt = std::max(1, (M + 16 * kIndexThreads - 1) / (16 * kIndexThreads));
+  const int chunks = (M + kIndexThreads * ix.tpt - 1) / (kIndexThreads * ix.tpt);
+  if (chunks > kIndexMaxChunks) return fail(COMET_EINVAL, "M=%d too large for the index build", M);
+  const int grid = std::min(x->n_sm, std::max(32, x->E_r * chunks));
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(index_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIndexSmem));
     attr_set = true;
   }
-  CK(cudaMemsetAsync(x->ix.transfer, 0, sizeof(int32_t) * c.world * c.world, static_cast<cudaStream_t>(stream)));
-  index_build_kernel<<<x->E_r + 1, kIndexThreads, kIndexSmem, static_cast<cudaStream_t>(stream)>>>(ix);
+  // global histogram + transfer matrix accumulate by atomics: zero both (adjacent)
+  const size_t zbytes = reinterpret_cast<char*>(x->ix.transfer + c.world * c.world) - reinterpret_cast<char*>(x->ix.counts);
+  CK(cudaMemsetAsync(x->ix.counts, 0, zbytes, static_cast<cudaStream_t>(stream)));
+  index_build_kernel<<<grid, kIndexThreads, kIndexSmem, static_cast<cudaStream_t>(stream)>>>(ix);
   CK(cudaGetLastError());
   x->ix.experts = d_experts;  // the layer1 finish kernel reads the global routing
   return COMET_OK;
@@ -714,12 +723,12 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
                   const float* combine_w, void* y_local, int activation, int n_comm0, int n_comm1, int group0,
                   int wave1, void* stream) {
   // hot path: no reference-format tile lists; combine list only for comm-CTA combine
-  const int flags = (x->cfg.world > 1 || n_comm1 > 0) ? kIndexCombineList : 0;
+  // (the combine list only feeds world-1 combine CTAs; world > 1 fuses the combine)
+  const int flags = (x->cfg.world == 1 && n_comm1 > 0 ? kIndexCombineList : 0) |
+                    (x->cfg.world > 1 ? kIndexSignal : 0);
   if (int rc = comet_index_build_ex(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), flags,
                                     stream))
     return rc;
-  if (x->cfg.world > 1)
-    if (int rc = comet_signal_tokens_ready(x, stream)) return rc;
   if (int rc = comet_layer0(x, w0t, activation, n_comm0, group0, stream)) return rc;
   if (int rc = comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream)) return rc;
   return comet_combine_finish(x, y_local, stream);

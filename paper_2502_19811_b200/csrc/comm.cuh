@@ -111,29 +111,35 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
   const int P = p.meta[kMetaPairs];
   const int n_tiles = 2 * P;
   if (warp == 0) {
-    // ---- loader warp ----
+    // ---- loader warp: lane-parallel index loads for 32 rows, then lane 0
+    // issues them in job order (slot waits never couple lanes of one batch) ----
     uint64_t ready_mask = 1ull << p.rank;
     int k = 0;
     for (int q = cid; q < n_tiles; q += n_comm) {
       int padrow0, nr;
       if (!remote_rows(p, q, padrow0, nr)) continue;
-      for (int r0 = 0; r0 < nr; r0 += kBatch) {
+      for (int r0 = 0; r0 < nr; r0 += 32) {
         const int r = r0 + lane;
-        if (lane < kBatch && r < nr) {
-          const int t = p.gather_row[padrow0 + r];
-          const int src = src_rank_of(t, p.M, p.world);
-          if (!((ready_mask >> src) & 1)) {
-            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + src), p.epoch)) __nanosleep(64);
-            ready_mask |= 1ull << src;
+        const int t = r < nr ? p.gather_row[padrow0 + r] : 0;
+        const int src = src_rank_of(t, p.M, p.world);
+        const int nb = min(32, nr - r0);
+        for (int i = 0; i < nb; ++i) {
+          const int ti = __shfl_sync(0xffffffffu, t, i);
+          const int si = __shfl_sync(0xffffffffu, src, i);
+          if (lane == 0) {
+            if (!((ready_mask >> si) & 1)) {
+              while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
+              ready_mask |= 1ull << si;
+            }
+            const int job = k + i;
+            const int slot = job % n_slots;
+            ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(cs->full + slot, row_bytes);
+            ptx::bulk_load(smem + slot * row_bytes, cs->xs_peer[si] + static_cast<long long>(ti) * p.n_embed,
+                           row_bytes, cs->full + slot);
           }
-          const int job = k + lane;
-          const int slot = job % n_slots;
-          ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(cs->full + slot, row_bytes);
-          ptx::bulk_load(smem + slot * row_bytes, cs->xs_peer[src] + static_cast<long long>(t) * p.n_embed,
-                         row_bytes, cs->full + slot);
         }
-        k += min(kBatch, nr - r0);
+        k += nb;
         __syncwarp();
       }
     }

@@ -22,12 +22,16 @@ enum MetaSlot : int {
   kMetaTiles1 = 5,     // reference layer1 tiles (= chunks * tiles per chunk)
   kMetaChunks = 6,     // reference reduce chunks
   kMetaCombineTok = 7, // tokens with at least one hosted expert
+  // 8..13: build phase timing probes (ns from kernel entry; CTA 0: phase 1a,
+  // 1b, grid barrier, phase 2; last CTA: phase 3 start, end), 15: overflow flags
   kMetaSlots = 16
 };
 
 // IndexDev::flags: what the last CTA emits besides the pair tables.
 constexpr int kIndexRefLists = 1;      // reference tiles0 / tiles1 / chunks (resolver API)
 constexpr int kIndexCombineList = 2;   // combine token list (comm-CTA combine)
+constexpr int kIndexSignal = 4;        // publish this rank's x_ready epoch to every peer
+constexpr int kIndexMaxChunks = 64;    // token chunks per hosted expert (host-checked)
 
 struct IndexDev {
   // inputs
@@ -37,6 +41,9 @@ struct IndexDev {
   int tile_rows, tile_cols, n_embed;
   int flags;
   int mloc_cap;             // combine slots per sender in the symmetric combine buffer
+  int tpt;                  // rotated token positions per thread per chunk (chunk = 1024 * tpt)
+  uint32_t epoch;
+  uint32_t* const* x_ready_peer;  // [world] peers' x_ready arrays (kIndexSignal)
 
   // outputs (device)
   int32_t* counts;      // [E]
@@ -61,10 +68,11 @@ struct IndexDev {
   int32_t* row_widx;    // [Rpad] t * topk + slot of the padded row (combine weight index)
   int32_t* meta;        // [kMetaSlots]
   // scratch
-  int32_t* first_key;   // [M]  demand key per token (INT_MAX = not needed)
-  int32_t* key_slot;    // [Rpad] token by demand key
   int32_t* pair_key;    // [P_cap]
   uint32_t* done;       // [1] CTA completion counter (self-resetting)
+  uint32_t* gbar;       // [2] grid barrier: arrival count (self-resetting), generation
+  int32_t* chunk_cnt;   // [E_r * kIndexMaxChunks] hits per (hosted expert, token chunk)
+  int32_t* chunk_loc;   // [E_r * kIndexMaxChunks] local-token hits per (hosted expert, chunk)
   uint32_t* zero_words; // layer1 per-n-block counters, zeroed every build
   int n_zero_words;
 

@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "index.cuh"
+#include "ptx.cuh"
 
 namespace comet {
 
@@ -71,12 +72,6 @@ __device__ __forceinline__ void warp_add(int* base, int idx, bool active) {
   if ((threadIdx.x & 31) == leader) atomicAdd(base + idx, __popc(peers));
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 __device__ __forceinline__ int slot_of(const int32_t* row, int topk, int e) {
   for (int s = 0; s < topk; ++s)
     if (row[s] == e) return s;
@@ -88,128 +83,103 @@ __device__ __forceinline__ long long tile_key(int ndeps, int e, int row_start) {
          static_cast<long long>(row_start);
 }
 
+
+// Token-chunk hits of hosted expert e: thread `tid` owns the rotated
+// positions [c*T + tid*TPT, +TPT) (contiguous rows -> coalesced warp loads).
+// Bit q of the result: position tid*TPT+q routes to e.
+__device__ __forceinline__ uint64_t chunk_hits(const IndexDev& ix, int c, int T, int TPT, int e, int start,
+                                               int n_own, int* n_loc) {
+  const int M = ix.M, K = ix.topk;
+  uint64_t hit = 0;
+  int loc = 0;
+#pragma unroll 4
+  for (int q = 0; q < TPT; ++q) {
+    const int i = c * T + threadIdx.x * TPT + q;
+    int t = start + i;
+    if (t >= M) t -= M;
+    const bool f = i < M && slot_of(ix.experts + static_cast<long long>(min(t, M - 1)) * K, K, e) >= 0;
+    hit |= static_cast<uint64_t>(f) << q;
+    loc += (f && i < n_own);
+  }
+  *n_loc = loc;
+  return hit;
+}
+
+// Grid-wide barrier for the (co-resident, <= one CTA per SM) index grid:
+// generation counter, self-resetting arrival count.
+__device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t g = *reinterpret_cast<volatile uint32_t*>(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *reinterpret_cast<volatile uint32_t*>(count) = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*reinterpret_cast<volatile uint32_t*>(gen) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
-  extern __shared__ long long sh_keys[];  // kSortSmemKeys (phase 2 only)
-  __shared__ int s_cnt[kMaxExperts];
+  extern __shared__ long long sh_keys[];  // kSortSmemKeys (bookkeeping scratch, phase 3 keys)
+  __shared__ int s_cnt[kMaxExperts];      // hosted expert totals, j-indexed
   __shared__ int s_off[kMaxExperts + 1];
   __shared__ int s_pad[kMaxExperts + 1];
   __shared__ int s_ws[kWarps];
   __shared__ int s_misc[8];
 
   const int tid = threadIdx.x;
+  unsigned long long tt0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));
+  auto probe = [&](int k) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (tid == 0 && (blockIdx.x == 0 || k >= 4)) ix.meta[8 + k] = (int)(t1 - tt0);
+  };
   const int M = ix.M, K = ix.topk, W = ix.world, E = ix.E, Er = ix.E_r;
-  const unsigned long long t_enter = globaltimer_ns();
-
-  // -------- phase 0 (every CTA): global histogram + hosted offsets --------
-  for (int e = tid; e < E; e += kThreads) s_cnt[e] = 0;
-  __syncthreads();
-  {
-    // batched coalesced loads (8 in flight per thread), then aggregated adds
-    constexpr int kB = 8;
-    for (int i0 = 0; i0 < M * K; i0 += kThreads * kB) {
-      int v[kB];
-#pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        const int i = i0 + b * kThreads + tid;
-        v[b] = i < M * K ? __ldg(ix.experts + i) : -1;
-      }
-#pragma unroll
-      for (int b = 0; b < kB; ++b) warp_add(s_cnt, max(v[b], 0), v[b] >= 0);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int o = 0, p = 0;
-    for (int j = 0; j < Er; ++j) {
-      s_off[j] = o;
-      s_pad[j] = p;
-      const int c = s_cnt[ix.e_lo + j];
-      o += c;
-      p += (c + kPairRows - 1) / kPairRows * kPairRows;
-    }
-    s_off[Er] = o;
-    s_pad[Er] = p;
-  }
-  __syncthreads();
-
+  const int TPT = ix.tpt, T = kThreads * TPT;
+  const int C = (M + T - 1) / T;  // token chunks (rotated order)
+  const int items = Er * C;       // (hosted expert, chunk) work items
   const int start = token_start_of(ix.rank, M, W);
   const int n_own = token_stop_of(ix.rank, M, W) - start;
 
-  const unsigned long long t_hist = globaltimer_ns();
-  if (blockIdx.x < Er) {
-    // -------- per-expert layout: rotated-token stream compaction --------
-    // Thread t owns the contiguous rotated positions [t*per, (t+1)*per):
-    // one batch of independent loads, one block scan for the thread offsets.
-    const int j = blockIdx.x, e = ix.e_lo + j;
-    const int base_row = s_off[j], base_pad = s_pad[j];
-    const int per = (M + kThreads - 1) / kThreads;
-    constexpr int kMaxPer = 64;  // tokens per thread (host guarantees M <= 64K)
-    int running = 0, n_loc = 0;
-    {
-      const int pass0 = 0;
-      const int cnt_pass = per;
-      uint64_t hit = 0;  // bit q: rotated position tid*per+q routes to e (per <= 64)
-      int mine_loc = 0;
-#pragma unroll 8
-      for (int q = 0; q < cnt_pass; ++q) {  // predicated (no early exit): loads batch up
-        const int i = tid * per + pass0 + q;
-        int t = start + i;
-        if (t >= M) t -= M;
-        const bool f = i < M && slot_of(ix.experts + static_cast<long long>(min(t, M - 1)) * K, K, e) >= 0;
-        hit |= static_cast<uint64_t>(f) << q;
-        mine_loc += (f && i < n_own);
-      }
-      int tot;
-      int pos = running + block_scan(__popcll(hit), s_ws, &tot);
-      while (hit) {
-        const int q = __ffsll(hit) - 1;
-        hit &= hit - 1;
-        const int i = tid * per + pass0 + q;
-        int t = start + i;
-        if (t >= M) t -= M;
-        const int32_t* trow = ix.experts + static_cast<long long>(t) * K;
-        const int sl = slot_of(trow, K, e);
-        if (base_pad + pos < ix.cap_rows_pad) {
-          // the token's last hosted expert (ascending slots) carries the fused
-          // combine: its epilogue folds the earlier hosted rows in
-          bool last = true;
-          for (int s2 = sl + 1; s2 < K; ++s2) last &= !(trow[s2] >= ix.e_lo && trow[s2] < ix.e_lo + Er);
-          const int sr = src_rank_of(t, M, W);
-          const int slot = (W > 1 ? ix.rank * ix.mloc_cap : 0) + t - token_start_of(sr, M, W);
-          ix.row_dst[base_pad + pos] = last ? ((sr << 24) | slot) : -1;
-          ix.row_widx[base_pad + pos] = t * K + sl;
-        }
-        if (base_row + pos < ix.cap_rows) {
-          ix.row_token[base_row + pos] = t;
-          ix.row_src[base_row + pos] = src_rank_of(t, M, W);
-        }
-        if (base_pad + pos < ix.cap_rows_pad) ix.gather_row[base_pad + pos] = t;
-        ix.tok_pos[static_cast<long long>(t) * K + sl] = base_pad + pos;
-        ++pos;
-      }
-      running += tot;
-      n_loc += mine_loc;
-    }
-    // local rows are exactly the rotated prefix [0, n_own)
-    int tot;
-    block_scan(n_loc, s_ws, &tot);
-    if (tid == 0) ix.n_local[j] = tot;
-    for (int r = base_pad + running + tid; r < s_pad[j + 1]; r += kThreads)
-      if (r < ix.cap_rows_pad) {
-        ix.gather_row[r] = -1;
-        ix.row_dst[r] = -1;
-        ix.row_widx[r] = 0;
-      }
+  // "my tokens are in place, my previous forward is done" -> every peer
+  // (index.cuh kIndexSignal; replaces a separate signal launch)
+  if ((ix.flags & kIndexSignal) && blockIdx.x == 0 && tid >= 32 && tid < 32 + W) {
+    ptx::fence_acq_rel_sys();
+    ptx::st_release_sys(ix.x_ready_peer[tid - 32] + ix.rank, ix.epoch);
   }
+  if (blockIdx.x == 0)
+    for (int i = tid; i < ix.n_zero_words; i += kThreads) ix.zero_words[i] = 0u;
+
+  // -------- phase 1a: per-(expert, chunk) hit counts --------
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int j = it / C, c = it - (it / C) * C;
+    int loc;
+    const uint64_t hit = chunk_hits(ix, c, T, TPT, ix.e_lo + j, start, n_own, &loc);
+    int tot, tot_loc;
+    block_scan(__popcll(hit), s_ws, &tot);
+    block_scan(loc, s_ws, &tot_loc);
+    if (tid == 0) {
+      ix.chunk_cnt[it] = tot;
+      ix.chunk_loc[it] = tot_loc;
+    }
+  }
+  probe(0);
+  // -------- phase 1b: bookkeeping over natural token slices: global
+  // histogram (routing.py:78-84), transfer matrix (routing.py:106-117) and
+  // the non-hosted tok_pos slots --------
   {
-    // -------- bookkeeping, split over every CTA (contiguous token slices):
-    // transfer matrix partials (routing.py:106-117) and the non-hosted slots
     int* s_tr = reinterpret_cast<int*>(sh_keys);  // W*W <= 4096 ints (host-checked)
-    if (blockIdx.x == gridDim.x - 1)
-      for (int e = tid; e < E; e += kThreads) ix.counts[e] = s_cnt[e];
+    int* s_hist = s_tr + W * W;                   // E <= 1024 ints
     for (int i = tid; i < W * W; i += kThreads) s_tr[i] = 0;
+    for (int i = tid; i < E; i += kThreads) s_hist[i] = 0;
     __syncthreads();
     const int per_group = E / ix.ep;
     const int t_lo = static_cast<int>(static_cast<long long>(M) * blockIdx.x / gridDim.x);
@@ -221,20 +191,98 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       for (int sl = 0; sl < K; ++sl) {
         const int e = ok ? __ldg(ix.experts + static_cast<long long>(t) * K + sl) : 0;
         const int g = e / per_group;
+        warp_add(s_hist, e, ok);
         for (int d = 0; d < ix.tp; ++d) warp_add(s_tr, src * W + g * ix.tp + d, ok);
         if (ok && (e < ix.e_lo || e >= ix.e_lo + Er)) ix.tok_pos[static_cast<long long>(t) * K + sl] = -1;
       }
     }
-    for (int i = tid; i < ix.n_zero_words; i += kThreads)
-      if (blockIdx.x == 0) ix.zero_words[i] = 0u;
     __syncthreads();
     for (int i = tid; i < W * W; i += kThreads)
       if (s_tr[i]) atomicAdd(ix.transfer + i, s_tr[i]);  // zeroed by the host before launch
+    for (int i = tid; i < E; i += kThreads)
+      if (s_hist[i]) atomicAdd(ix.counts + i, s_hist[i]);
   }
 
+  probe(1);
+  grid_barrier(ix.gbar, ix.gbar + 1);
+  probe(2);
+
+  // -------- phase 2: hosted offsets (every CTA), then stable compaction --------
+  for (int j = tid; j < Er; j += kThreads) {
+    int t = 0;
+    for (int c = 0; c < C; ++c) t += __ldcg(ix.chunk_cnt + j * C + c);
+    s_cnt[j] = t;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0, pd = 0;
+    for (int j = 0; j < Er; ++j) {
+      s_off[j] = o;
+      s_pad[j] = pd;
+      o += s_cnt[j];
+      pd += (s_cnt[j] + kPairRows - 1) / kPairRows * kPairRows;
+    }
+    s_off[Er] = o;
+    s_pad[Er] = pd;
+  }
+  __syncthreads();
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int j = it / C, c = it - (it / C) * C, e = ix.e_lo + j;
+    if (tid == 0) {
+      int before = 0;
+      for (int c2 = 0; c2 < c; ++c2) before += __ldcg(ix.chunk_cnt + j * C + c2);
+      s_misc[0] = before;
+      if (c == 0) {
+        int nl = 0;
+        for (int c2 = 0; c2 < C; ++c2) nl += __ldcg(ix.chunk_loc + j * C + c2);
+        ix.n_local[j] = nl;
+      }
+    }
+    int loc;
+    uint64_t hit = chunk_hits(ix, c, T, TPT, e, start, n_own, &loc);
+    int tot;
+    const int mine = block_scan(__popcll(hit), s_ws, &tot);  // (syncs: s_misc visible)
+    const int base_row = s_off[j], base_pad = s_pad[j];
+    int pos = s_misc[0] + mine;
+    while (hit) {
+      const int q = __ffsll(hit) - 1;
+      hit &= hit - 1;
+      const int i = c * T + tid * TPT + q;
+      int t = start + i;
+      if (t >= M) t -= M;
+      const int32_t* trow = ix.experts + static_cast<long long>(t) * K;
+      const int sl = slot_of(trow, K, e);
+      if (base_pad + pos < ix.cap_rows_pad) {
+        // the token's last hosted expert (ascending slots) carries the fused
+        // combine: its epilogue folds the earlier hosted rows in
+        bool last = true;
+        for (int s2 = sl + 1; s2 < K; ++s2) last &= !(trow[s2] >= ix.e_lo && trow[s2] < ix.e_lo + Er);
+        const int sr = src_rank_of(t, M, W);
+        const int slot = (W > 1 ? ix.rank * ix.mloc_cap : 0) + t - token_start_of(sr, M, W);
+        ix.row_dst[base_pad + pos] = last ? ((sr << 24) | slot) : -1;
+        ix.row_widx[base_pad + pos] = t * K + sl;
+        ix.gather_row[base_pad + pos] = t;
+      }
+      if (base_row + pos < ix.cap_rows) {
+        ix.row_token[base_row + pos] = t;
+        ix.row_src[base_row + pos] = src_rank_of(t, M, W);
+      }
+      ix.tok_pos[static_cast<long long>(t) * K + sl] = base_pad + pos;
+      ++pos;
+    }
+    if (c == C - 1)  // padding rows of expert j's 256-aligned block
+      for (int r = base_pad + s_cnt[j] + tid; r < s_pad[j + 1]; r += kThreads)
+        if (r < ix.cap_rows_pad) {
+          ix.gather_row[r] = -1;
+          ix.row_dst[r] = -1;
+          ix.row_widx[r] = 0;
+        }
+    __syncthreads();  // s_misc reuse
+  }
+
+  probe(3);
   // -------- grid completion: the last CTA builds the schedules --------
   __syncthreads();
-  const unsigned long long t_phase1 = globaltimer_ns();
   if (tid == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(ix.done, 1u);
@@ -243,21 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   __syncthreads();
   if (!s_misc[1]) return;
   __threadfence();
-
-  // recompute hosted offsets (s_off may have been reused as scratch)
-  if (tid == 0) {
-    int o = 0, p = 0;
-    for (int j = 0; j < Er; ++j) {
-      s_off[j] = o;
-      s_pad[j] = p;
-      const int c = s_cnt[ix.e_lo + j];
-      o += c;
-      p += (c + kPairRows - 1) / kPairRows * kPairRows;
-    }
-    s_off[Er] = o;
-    s_pad[Er] = p;
-  }
-  __syncthreads();
+  probe(4);
   for (int j = tid; j <= Er; j += kThreads) {
     ix.row_off[j] = s_off[j];
     ix.pad_off[j] = s_pad[j];
@@ -275,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     for (int j = 0; j < Er; ++j) {
       s_t0[j] = t;
       s_p0[j] = p;
-      const int c = s_cnt[ix.e_lo + j];
+      const int c = s_cnt[j];
       t += (c + TR - 1) / TR;
       p += (c + kPairRows - 1) / kPairRows;
     }
@@ -287,7 +321,6 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   const bool ovf = T0 > ix.cap_tiles0 || P > ix.cap_pairs || s_pad[Er] > ix.cap_rows_pad ||
                    s_off[Er] > ix.cap_rows;
 
-  const unsigned long long t_p2a = globaltimer_ns();
   // ---- layer0 tiles sorted by (n_deps, expert, row_start) ----
   auto tile_of = [&](int idx, int& j, int& rs, int& re, int& nd) {
     int lo = 0, hi = Er - 1;  // expert with s_t0[j] <= idx < s_t0[j+1]
@@ -296,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       if (s_t0[mid] <= idx) lo = mid; else hi = mid - 1;
     }
     j = lo;
-    const int c = s_cnt[ix.e_lo + j];
+    const int c = s_cnt[j];
     rs = (idx - s_t0[j]) * TR;
     re = min(rs + TR, c);
     const int loc_end = min(re, s_nloc[j]);
@@ -334,12 +367,11 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     }
   }
   __syncthreads();
-  const unsigned long long t_p2b = globaltimer_ns();
 
   // ---- layer1 reference tiles: column block outer, (expert,row) inner ----
   const int TC = ix.tile_cols, NE = ix.n_embed;
-  const int C = (NE + TC - 1) / TC;
-  const long long T1 = static_cast<long long>(C) * T0;
+  const int NCH = (NE + TC - 1) / TC;
+  const long long T1 = static_cast<long long>(NCH) * T0;
   const bool ovf1 = emit_lists && T1 > ix.cap_tiles1;
   int4* s_tile = reinterpret_cast<int4*>(sh_keys);  // per-tile (expert, rs, re, nd) cache
   const bool tiles_in_smem = T0 <= kSortSmemKeys / 2;
@@ -366,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       o[0] = tq.x; o[1] = tq.y; o[2] = tq.z;
       o[3] = c * TC; o[4] = min(c * TC + TC, NE); o[5] = tq.w;
     }
-    for (int c = tid; c < C; c += kThreads) {
+    for (int c = tid; c < NCH; c += kThreads) {
       int* o = ix.chunks + c * 4;
       o[0] = c * TC; o[1] = min(c * TC + TC, NE); o[2] = c * T0; o[3] = T0;
     }
@@ -383,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       if (s_p0[mid] <= idx) lo = mid; else hi = mid - 1;
     }
     j = lo;
-    const int c = s_cnt[ix.e_lo + j];
+    const int c = s_cnt[j];
     const int r0 = (idx - s_p0[j]) * kPairRows;
     prow = s_pad[j] + r0;
     valid = min(kPairRows, c - r0);
@@ -392,7 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     const int nd = (last_re - last_rs) - max(0, min(last_re, s_nloc[j]) - last_rs);
     key = tile_key(nd, ix.e_lo + j, last_rs);
   };
-  const unsigned long long t_p2c = globaltimer_ns();
   long long* s_pkey = sh_keys;  // P keys (P <= kSortSmemKeys, else recomputed)
   const bool pkeys_in_smem = P <= kSortSmemKeys;
   if (!ovf) {
@@ -424,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       ix.pair_key[i] = rank;
       // .w: bit h set when 128-row half h holds rows pulled from other ranks
       const int r0 = prow - s_pad[j];
-      const int remote_mask = (min(r0 + kTileRows, s_cnt[ix.e_lo + j]) > s_nloc[j] ? 1 : 0) |
+      const int remote_mask = (min(r0 + kTileRows, s_cnt[j]) > s_nloc[j] ? 1 : 0) |
                               (valid > kTileRows && r0 + valid > s_nloc[j] ? 2 : 0);
       o[0] = j; o[1] = prow; o[2] = valid; o[3] = remote_mask;
       int* o0 = ix.pairs0 + rank * 4;
@@ -437,7 +468,6 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   if (tid == 0) s_misc[2] = 0;  // pull list retired: remote rows are pulled per tile (comm.cuh)
   __syncthreads();
 
-  const unsigned long long t_p2d = globaltimer_ns();
   // ---- combine token list: tokens with >=1 hosted expert, ascending ----
   if (ix.flags & kIndexCombineList) {
     const int per = (M + kThreads - 1) / kThreads;
@@ -465,22 +495,15 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   }
   __syncthreads();
 
+  probe(5);
   if (tid == 0) {
-    const unsigned long long t_end = globaltimer_ns();
-    ix.meta[8] = static_cast<int>(t_hist - t_enter);
-    ix.meta[9] = static_cast<int>(t_phase1 - t_enter);
-    ix.meta[10] = static_cast<int>(t_end - t_enter);
-    ix.meta[11] = static_cast<int>(t_p2a - t_enter);
-    ix.meta[12] = static_cast<int>(t_p2b - t_enter);
-    ix.meta[13] = static_cast<int>(t_p2c - t_enter);
-    ix.meta[14] = static_cast<int>(t_p2d - t_enter);
     ix.meta[kMetaRows] = s_off[Er];
     ix.meta[kMetaRowsPad] = Rpad;
     ix.meta[kMetaTiles0] = T0;
     ix.meta[kMetaPairs] = P;
     ix.meta[kMetaPull] = ovf ? 0 : s_misc[2];
     ix.meta[kMetaTiles1] = static_cast<int>(T1);
-    ix.meta[kMetaChunks] = C;
+    ix.meta[kMetaChunks] = NCH;
     ix.meta[kMetaCombineTok] = s_misc[3];
     ix.meta[kMetaSlots - 1] = (ovf ? 1 : 0) | (ovf1 ? 2 : 0);
     *ix.done = 0u;  // self-reset for the next launch

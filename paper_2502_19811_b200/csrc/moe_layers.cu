@@ -418,7 +418,9 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
 
 // Final combine on the source rank (world > 1): sum the partial rows pushed by
 // every contributing rank, ascending rank order (executor.py:239-245 for TP,
-// 102-120 for experts split across EP groups).
+// 102-120 for experts split across EP groups).  One warp per token: the
+// contributor list is built once, then every lane streams 16 B columns of all
+// contributors with several loads in flight.
 __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb,
                                                              const uint32_t* cb_flag, const int32_t* experts) {
   const int NB = p.n_blocks, N = p.n_embed, K = p.topk, W = p.world;
@@ -427,37 +429,55 @@ __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, 
   for (int i = threadIdx.x; i < W * NB; i += blockDim.x)
     while (!ptx::epoch_reached(ptx::ld_acquire_sys(cb_flag + i), p.epoch)) __nanosleep(64);
   __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int vec = N / 8;
-  const long long n_items = static_cast<long long>(n_own) * vec;
-  for (long long it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items;
-       it += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int lt = static_cast<int>(it / vec), c = static_cast<int>(it % vec) * 8;
+  constexpr int kU = 4;
+  for (int lt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; lt < n_own; lt += (gridDim.x * blockDim.x) >> 5) {
     const int t = start + lt;
     // contributing ranks: every TP rank of each distinct EP group of t's
-    // experts, visited in ascending rank order
-    float acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    int last_group = -1;
+    // experts (ascending experts -> ascending groups -> ascending ranks)
+    const int ge = lane < K ? experts[static_cast<long long>(t) * K + lane] / p.experts_per_group : -1;
+    int groups[8];
+    int ng = 0, last = -1;
     for (int s = 0; s < K; ++s) {
-      const int g = experts[static_cast<long long>(t) * K + s] / p.experts_per_group;
-      if (g == last_group) continue;
-      last_group = g;
-      for (int r = g * p.tp; r < (g + 1) * p.tp; ++r) {
-        const uint4 v = ptx::ld_v4(cb + (static_cast<long long>(r) * p.mloc_cap + lt) * N + c);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+      const int g = __shfl_sync(0xffffffffu, ge, s);
+      if (g != last) groups[ng++] = g;
+      last = g;
+    }
+    for (int c0 = lane; c0 < vec; c0 += 32 * kU) {
+      float acc[kU][8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(h[j]);
-          acc[2 * j] += f.x;
-          acc[2 * j + 1] += f.y;
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[u][j] = 0.f;
+      for (int gi = 0; gi < ng; ++gi) {
+        for (int r = groups[gi] * p.tp; r < (groups[gi] + 1) * p.tp; ++r) {
+          const __nv_bfloat16* row = cb + (static_cast<long long>(r) * p.mloc_cap + lt) * N;
+          uint4 v[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            v[u] = c0 + u * 32 < vec ? ptx::ld_v4(row + (c0 + u * 32) * 8) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = __bfloat1622float2(h[j]);
+              acc[u][2 * j] += f.x;
+              acc[u][2 * j + 1] += f.y;
+            }
+          }
         }
       }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (c0 + u * 32 >= vec) continue;
+        uint4 o;
+        o.x = pack_bf16(acc[u][0], acc[u][1]); o.y = pack_bf16(acc[u][2], acc[u][3]);
+        o.z = pack_bf16(acc[u][4], acc[u][5]); o.w = pack_bf16(acc[u][6], acc[u][7]);
+        ptx::st_v4(p.y_local + static_cast<long long>(lt) * N + (c0 + u * 32) * 8, o);
+      }
     }
-    uint4 o;
-    o.x = pack_bf16(acc[0], acc[1]); o.y = pack_bf16(acc[2], acc[3]);
-    o.z = pack_bf16(acc[4], acc[5]); o.w = pack_bf16(acc[6], acc[7]);
-    ptx::st_v4(p.y_local + static_cast<long long>(lt) * N + c, o);
   }
 }
 

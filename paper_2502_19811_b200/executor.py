@@ -319,6 +319,12 @@ def run_emulated(x, weights: ExpertWeights, routing: RoutingTable, parallel: Par
     return out[:, :model.N].float()
 
 
+def index_flags(world: int, n_comm1: int) -> int:
+    """Index-build flags of the forward hot path (index.cuh): combine token
+    list only for world-1 combine CTAs; x_ready signal when world > 1."""
+    return (2 if world == 1 and n_comm1 > 0 else 0) | (4 if world > 1 else 0)
+
+
 def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
     """Enqueue a forward of every emulated rank, phase by phase, on one
     stream: each in-kernel wait is on work enqueued before it, so ranks that
@@ -326,12 +332,9 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
     layer1 -> remote combine)."""
     world = layers[0].parallel.world_size
     for layer in layers:
-        # hot path: the kernels' tables only (+ the combine list for comm-CTA combine)
-        flags = 2 if (world > 1 or layer.knobs.n_comm1 > 0) else 0
-        layer.ctx.index_build(ex, M, stream=stream, flags=flags)
-    if world > 1:
-        for layer in layers:
-            layer.ctx.signal_tokens_ready(stream=stream)
+        # hot path: the kernels' tables only (+ the combine list for world-1
+        # combine CTAs); world > 1: the build also publishes the x_ready epoch
+        layer.ctx.index_build(ex, M, stream=stream, flags=index_flags(world, layer.n_comm1()))
     for layer in layers:
         k = layer.knobs
         layer.ctx.layer0(layer.weights.w0t, layer.act, k.n_comm0 if world > 1 else 0, k.group0, stream=stream)

@@ -7,7 +7,7 @@ from paper_2502_19811_b200 import LayerKnobs, ModelConfig, ParallelSpec, Workloa
 from paper_2502_19811_b200.executor import MoELayer, RankWeights, _lib
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-nc0 = int(os.environ.get("NC0", 2)); nc1 = int(os.environ.get("NC1", 4))
+nc0 = int(os.environ.get("NC0", 2)); nc1 = int(os.environ.get("NC1", 0)); g0 = int(os.environ.get("G0", 4))
 E, topk, N, K, M = 8, 2, 4096, 14336, 8192
 model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
 par = ParallelSpec(1, W)
@@ -28,15 +28,15 @@ for l in layers:
     l.place_tokens(x[lo:hi], M)
     ys.append(torch.empty(hi - lo, N, dtype=torch.bfloat16, device="cuda"))
 ev = lambda: torch.cuda.Event(enable_timing=True)
-res = {k: [] for k in ("index", "layer0", "layer1", "finish")}
+res = {k: [] for k in ("index", "layer0", "layer1", "finish", "total")}
 for it in range(6):
+    ti = []
     for l in layers:
-        l.ctx.index_build(ex, M, flags=2)
-    for l in layers:
-        l.ctx.signal_tokens_ready()
+        a, b = ev(), ev(); a.record(); l.ctx.index_build(ex, M, flags=4); b.record()
+        ti.append((a, b))
     t = []
     for l in layers:
-        a, b = ev(), ev(); a.record(); l.ctx.layer0(l.weights.w0t, 0, nc0, 4); b.record(); t.append((a, b))
+        a, b = ev(), ev(); a.record(); l.ctx.layer0(l.weights.w0t, 0, nc0, g0); b.record(); t.append((a, b))
     t1 = []
     for l, y in zip(layers, ys):
         a, b = ev(), ev(); a.record(); l.ctx.layer1(l.weights.w1t, None, y, nc1, 4); b.record(); t1.append((a, b))
@@ -45,12 +45,14 @@ for it in range(6):
         a, b = ev(), ev(); a.record(); l.ctx.combine_finish(y); b.record(); t2.append((a, b))
     torch.cuda.synchronize()
     if it >= 2:
+        res["index"].append(max(a.elapsed_time(b) for a, b in ti))
         res["layer0"].append(max(a.elapsed_time(b) for a, b in t))
+        res["total"].append(max(sum(x[0].elapsed_time(x[1]) for x in xs) for xs in zip(ti, t, t1, t2)))
         res["layer1"].append(max(a.elapsed_time(b) for a, b in t1))
         res["finish"].append(max(a.elapsed_time(b) for a, b in t2))
 rows = layers[0].ctx.index_meta()[0]
 fl = 2.0 * rows * N * K / W * W  # per rank (tp=1): 2*rows*N*K
-print(f"EP={W} rank rows={rows}: layer0 {statistics.median(res['layer0']):.3f} ms, layer1 {statistics.median(res['layer1']):.3f} ms, "
+print(f"EP={W} rank rows={rows}: forward {statistics.median(res['total']):.3f} ms (index {statistics.median(res['index']):.3f}); layer0 {statistics.median(res['layer0']):.3f} ms, layer1 {statistics.median(res['layer1']):.3f} ms, "
       f"finish {statistics.median(res['finish']):.3f} ms (max over ranks); per-layer TF/s "
       f"{2.0*rows*N*K/statistics.median(res['layer0'])/1e9:.0f} / {2.0*rows*N*K/statistics.median(res['layer1'])/1e9:.0f}")
 
@@ -59,11 +61,9 @@ if os.environ.get("TL"):
     l0 = layers[0]
     l0.ctx.timeline_enable(256)
     for l in layers:
-        l.ctx.index_build(ex, M, flags=2)
+        l.ctx.index_build(ex, M, flags=4)
     for l in layers:
-        l.ctx.signal_tokens_ready()
-    for l in layers:
-        l.ctx.layer0(l.weights.w0t, 0, nc0, 4)
+        l.ctx.layer0(l.weights.w0t, 0, nc0, g0)
     torch.cuda.synchronize()
     for tag in ("layer0", "layer1"):
         if tag == "layer1":
