@@ -626,6 +626,10 @@ int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int 
   a.b_rows = x->k_local;
   a.order_group = group;
   a.activation = activation;
+  {
+    const char* sp = getenv("COMET_SPLIT");
+    a.split_tail = sp == nullptr || atoi(sp) != 0;
+  }
   a.pairs = x->ix.pairs0;
   a.out = x->H;
   a.out_ld = x->k_local;

@@ -27,6 +27,7 @@ struct LayerArgs {
   int order_group;        // layer0: pairs per group; layer1: n-blocks per wave
   int order_group2;       // layer1: pairs per group inside a wave
   int activation;
+  int split_tail;         // layer0: cut a mostly idle last round into 256-column half units
   uint32_t epoch;
   int debug;              // bit0: comm CTAs idle; bit1: layer0 A by 2D tile (no gather); bit2: spin waits
 

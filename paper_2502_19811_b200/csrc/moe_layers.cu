@@ -53,7 +53,22 @@ constexpr uint32_t kSmemEpi = 2 * 4 * kSmemEpiWarp;      // double-buffered, 4 e
 
 struct Unit {
   int pair, nb;
+  int half;  // -1: full 512-column unit; 0/1: one 256-column half (tail split)
 };
+
+// Tail split (layer0): when the last round of full units would leave at
+// least half the pairs idle, its units are cut into 256-column halves so the
+// tail takes half a unit time instead of a full one.  Units [0, R*n_pairs)
+// stay full; unit R*n_pairs + v is half (v & 1) of full unit R*n_pairs + v/2.
+struct Sched {
+  int full;   // full units before the tail
+  int total;  // units in the loop (full + halves)
+};
+__device__ __forceinline__ Sched make_sched(int U, int n_pairs, bool split) {
+  const int R = U / n_pairs, rem = U - R * n_pairs;
+  if (split && rem > 0 && 2 * rem <= n_pairs) return {R * n_pairs, R * n_pairs + 2 * rem};
+  return {U, U};
+}
 
 // Timeline record: interval [t0, t1] of `role` for unit `task` on this CTA
 // (globaltimer ns).  Exported as the reference simulator's timeline CSV
@@ -196,9 +211,22 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
 
   const int P = p.meta[kMetaPairs];
   const int NB = p.n_blocks;
-  const int U = P * NB;
   const int pair_id = blockIdx.x >> 1;
   const int n_pairs = p.n_compute >> 1;
+  const Sched sch = make_sched(P * NB, n_pairs, p.layer == 0 && p.split_tail);
+  const int U = sch.total;
+  auto unit_of = [&](int u) {
+    Unit w;
+    if (u < sch.full) {
+      w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
+      w.half = -1;
+    } else {
+      const int v = u - sch.full;
+      w = decode_unit(sch.full + (v >> 1), p.layer, P, NB, p.order_group, p.order_group2);
+      w.half = v & 1;
+    }
+    return w;
+  };
   if (p.layer == 1 && p.world > 1 && P == 0 && gridDim.x == static_cast<unsigned>(p.n_compute) &&
       blockIdx.x == 0 && threadIdx.x == 0)  // nothing hosted, no combine CTAs: publish empty blocks
     for (int nb = 0; nb < NB; ++nb)
@@ -210,10 +238,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     uint32_t phase = 0;
     int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const Unit w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
+      const Unit w = unit_of(u);
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
-      const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta);
+      const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta) + (w.half > 0 ? kHalfN : 0);
       if (p.layer == 0 && ((pr.w >> cta) & 1) && !(p.debug & 1) && lane == 0) {
         // this CTA's 128 A rows include rows pulled over NVLink by a comm CTA
         const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
@@ -232,9 +260,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           uint8_t* sa = smem + stage * kSmemStage;
           ptx::tma_load_2d_2sm(sa, &tm_a, full + stage, kb * kBlockK, row0, ptx::kEvictNormal);
           ptx::tma_load_2d_2sm(sa + kSmemA, &tm_b, full + stage, kb * kBlockK, brow, ptx::kEvictNormal);
-          ptx::tma_load_2d_2sm(sa + kSmemA + kSmemBh, &tm_b, full + stage, kb * kBlockK, brow + kHalfN,
-                               ptx::kEvictNormal);
-          if (leader) ptx::mbar_arrive_expect_tx(full + stage, 2 * kSmemStage);
+          if (w.half < 0)
+            ptx::tma_load_2d_2sm(sa + kSmemA + kSmemBh, &tm_b, full + stage, kb * kBlockK, brow + kHalfN,
+                                 ptx::kEvictNormal);
+          if (leader) ptx::mbar_arrive_expect_tx(full + stage, w.half < 0 ? 2 * kSmemStage : 2 * (kSmemA + kSmemBh));
           else ptx::mbar_arrive_cluster(full + stage, 0);
         }
         __syncwarp();
@@ -248,6 +277,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     uint32_t phase = 0;
     int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
+      const bool two = unit_of(u).half < 0;  // both accumulator halves (else only half 0)
       const uint32_t ephase = (it & 1) ^ 1;  // previous unit's drain of each half
       const uint64_t t_w = ptx::globaltimer();
       wait(tempty + 0, ephase);
@@ -272,7 +302,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           ptx::tc_fence_after();
         }
         if (lane == 0) {
-          if (!(p.debug & 8)) {
+          if (!(p.debug & 8) && two) {
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k)
               ptx::mma_bf16_2sm(tmem_base + kHalfN, da + 2 * k, db1 + 2 * k, kIdesc, (kb | k) != 0);
@@ -293,20 +323,22 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     const int ew = warp - 4;
     int it = 0;
     for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const Unit w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
+      const Unit w = unit_of(u);
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       wait(tfull, it & 1);
       ptx::tc_fence_after();
       const uint64_t t_e = ptx::globaltimer();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
-      const int cols_left = p.out_ld - w.nb * kBlockN;  // ragged last n-block (e.g. K/tp = 3200)
+      const int col0 = w.half > 0 ? static_cast<int>(kHalfN) : 0;           // tail half unit: its columns
+      const int cols_left = p.out_ld - w.nb * kBlockN - col0;  // ragged last n-block (e.g. K/tp = 3200)
+      const int n_chunks = w.half < 0 ? static_cast<int>(kBlockN / 64) : static_cast<int>(kHalfN / 64);
       // Destination of this lane's row: the layer output, or -- fused combine,
       // the row of its token's last hosted expert -- the token's weighted sum
       // over its hosted experts (executor.py:102-120), written to y (world 1)
       // or pushed straight into the source rank's combine slot over NVLink.
       const int my_row = row0 + ew * 32 + lane;
-      __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN;
+      __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN + col0;
       float scale = 1.f;
       int fold_t = -1, fold_s = 0;  // token and own slot of a last-hosted row
       if (p.layer == 1 && p.fuse_combine) {
@@ -330,13 +362,17 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
       }
       const unsigned long long my_addr = reinterpret_cast<unsigned long long>(my_dst);
 #pragma unroll 1
-      for (int s = 0; s < static_cast<int>(kBlockN / 64); ++s) {
+      for (int s = 0; s < n_chunks; ++s) {
         const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
         if (p.debug & 128) {  // debug: drain nothing
           if (half_end) {
             ptx::tc_fence_before();
             if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
             else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
+            if (w.half >= 0) {
+              if (leader) ptx::mbar_arrive(tempty + 1);
+              else ptx::mbar_arrive_cluster(tempty + 1, 0);
+            }
           }
           continue;
         }
@@ -346,9 +382,15 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         ptx::tmem_ld_wait();
         if (half_end) {
           // accumulator half drained: the next unit's MMAs may overwrite it
+          // (a tail half unit used only half 0: release both)
           ptx::tc_fence_before();
-          if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
-          else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
+          const int h = s * 64 >= static_cast<int>(kHalfN);
+          if (leader) ptx::mbar_arrive(tempty + h);
+          else ptx::mbar_arrive_cluster(tempty + h, 0);
+          if (w.half >= 0) {
+            if (leader) ptx::mbar_arrive(tempty + 1);
+            else ptx::mbar_arrive_cluster(tempty + 1, 0);
+          }
         }
         if (s * 64 >= cols_left || (p.debug & 64)) continue;
         if (p.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows

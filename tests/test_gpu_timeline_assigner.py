@@ -13,7 +13,13 @@ from paper_2502_19811_b200.executor import _group_cache, run_emulated
 pytestmark = pytest.mark.gpu
 
 
-def _decode_layer0(u, P, NB, G):
+def _decode_layer0(u, P, NB, G, n_pairs=None):
+    """Pair of layer0 unit u (moe_layers.cu decode_unit + make_sched tail split)."""
+    if n_pairs is not None:
+        U = P * NB
+        R, rem = divmod(U, n_pairs)
+        if rem and 2 * rem <= n_pairs and u >= R * n_pairs:
+            u = R * n_pairs + (u - R * n_pairs) // 2
     per_group = G * NB
     g = u // per_group
     ge = min(G, P - g * G)
@@ -60,8 +66,9 @@ def test_measured_timeline_overlap_and_dependency_audit():
         comm_ivs = [TL.Interval(c, "comm", t, s, e) for c, r, t, s, e in recs if r == "comm"]
         assert len({iv.task_id for iv in comm_ivs}) == len(comm_ivs)
         load_ivs = [TL.Interval(c, "compute", 2 * t + (c & 1), s, e) for c, r, t, s, e in recs if r == "load"]
-        deps = {2 * u + c: [2 * _decode_layer0(u, P, NB, knobs.group0) + c]
-                for u in range(P * NB) for c in (0, 1)}
+        n_pairs = (torch.cuda.get_device_properties(0).multi_processor_count // 2 * 2 - knobs.n_comm0) // 2
+        deps = {2 * u + c: [2 * _decode_layer0(u, P, NB, knobs.group0, n_pairs) + c]
+                for u in range(2 * P * NB) for c in (0, 1)}
         bad = [p for p in TL.audit(comm_ivs + load_ivs, deps) if "overlaps" not in p]
         assert bad == [], bad[:5]
     for layer, y in zip(layers, ys):
