@@ -153,6 +153,22 @@ int32_t comet_hidden_rows_cap(comet_ctx* ctx);
 int comet_timeline_enable(comet_ctx* ctx, int cap);
 int comet_timeline_dump(comet_ctx* ctx, void* host_buf, size_t cap_bytes);
 
+/* GPU router front-end (no context).  Gate logits [M, E] (logits_dtype 0 =
+ * fp32, 1 = bf16, row-major, device) -> d_experts [M, topk] int32, the top-k
+ * expert ids stored ASCENDING per token: the reference router-output layout
+ * RoutingTable.experts_per_token (routing.py:62-163, validated ascending and
+ * distinct at 146-163) that comet_index_build consumes.  Selection is a
+ * stable descending sort of the logits (ties -> smaller id, -0 == +0, NaN
+ * below -inf); indices are bit-exact with oracle/moe_oracle.router_topk.
+ * d_weights [M, topk] fp32 in the same ascending slot order -- the
+ * combine_weights of executor.py:102-120 -- for norm 1 (softmax over the k
+ * selected logits) or 2 (softmax over all E, selected entries); norm 0
+ * writes no weights (d_weights may be NULL).  E <= 512, topk <= min(E, 32).
+ * The reference has no router (build_routing, routing.py:283-307, is a
+ * synthetic count generator): this replaces the model's gate in front of it. */
+int comet_router_topk(const void* d_logits, int logits_dtype, int M, int E, int topk, int norm,
+                      int32_t* d_experts, float* d_weights, void* stream);
+
 /* Number of SMs and max co-resident 2-CTA clusters for the layer kernel. */
 int comet_device_info(int device, int32_t out[4]);
 

@@ -14,6 +14,13 @@ line range it follows under ``/root/reference/pkg/src/moepipe/``:
   ``expert_counts`` / ``transfer_counts`` (routing.py:78-117),
   ``sort_layout`` (resolver.py:171-195), ``layer0_tiles`` (resolver.py:206-252),
   ``layer1_tiles`` (resolver.py:255-309);
+* router front-end: ``router_topk`` -- gate logits ->
+  top-k expert ids stored ascending (the RoutingTable.experts_per_token
+  layout, routing.py:146-163) + softmax combine weights in the same slot
+  order (executor.py:102-120).  The reference has no router
+  (``build_routing``, routing.py:283-307, synthesises counts), so this one
+  is **parity unpinned** against the reference: it is defined here as a
+  stable descending argsort and pinned by construction-level checks only;
 * float path: ``layer_forward`` = ``execute_naive`` (executor.py:132-148) with
   ``_hidden_row`` (86-90), ``_output_columns`` (93-99) and ``_combine``
   (102-120) folded into one GEMM pair per expert; ``layer_forward_tp`` =
@@ -257,3 +264,38 @@ def relative_error(got: np.ndarray, ref: np.ndarray) -> Tuple[float, float]:
     fr = float(np.linalg.norm(ref)) if ref.size else 0.0
     return (float(np.abs(d).max()) / mx if mx else float(np.abs(d).max() if d.size else 0.0),
             float(np.linalg.norm(d)) / fr if fr else float(np.linalg.norm(d)))
+
+
+# ---------------------------------------------------------------------------
+# Router front-end (no reference counterpart: parity unpinned)
+# ---------------------------------------------------------------------------
+
+def router_topk(logits: np.ndarray, topk: int, norm: str = "topk") -> Tuple[np.ndarray, Optional[np.ndarray]]:
+    """Top-k experts per token, stored ascending (routing.py:146-163 layout).
+
+    Selection = stable descending argsort of the logits: larger logit first,
+    ties -> smaller expert id; -0.0 ties +0.0; NaN ranks below -inf.
+    Weights (float64) in ascending-expert slot order: ``"topk"`` softmax over
+    the selected logits, ``"all"`` softmax over all E logits (selected
+    entries), ``None`` no weights."""
+    lg = np.asarray(logits, dtype=np.float64)
+    M, E = lg.shape
+    key = np.where(np.isnan(lg), -np.inf, lg)
+    # rank NaN strictly below -inf: sort by (isnan, -key, id)
+    order = np.lexsort((np.broadcast_to(np.arange(E), (M, E)), -key, np.isnan(lg)), axis=1)
+    sel = order[:, :topk]
+    experts = np.sort(sel, axis=1).astype(np.int32)
+    if norm is None:
+        return experts, None
+    chosen = np.take_along_axis(lg, experts.astype(np.int64), axis=1)
+    if norm == "topk":
+        mx = chosen.max(axis=1, keepdims=True) if topk else 0.0
+        ex = np.exp(chosen - mx)
+        w = ex / ex.sum(axis=1, keepdims=True)
+    elif norm == "all":
+        mx = lg.max(axis=1, keepdims=True)
+        w = np.exp(chosen - mx) / np.exp(lg - mx).sum(axis=1, keepdims=True)
+    else:
+        raise ValueError(f"unknown norm {norm!r}")
+    return experts, w
+

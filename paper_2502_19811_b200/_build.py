@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcomet_b200.so")
-SOURCES = ["index_build.cu", "moe_layers.cu", "capi.cu"]
+SOURCES = ["index_build.cu", "moe_layers.cu", "router.cu", "capi.cu"]
 HEADERS = ["ptx.cuh", "index.cuh", "layers.cuh", "comm.cuh"]
 
 

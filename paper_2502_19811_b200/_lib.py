@@ -32,7 +32,7 @@ EXPORTS = (
     "comet_routing_buffer", "comet_index_build", "comet_index_build_ex", "comet_index_sizes", "comet_index_download",
     "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
-    "comet_timeline_enable", "comet_timeline_dump",
+    "comet_timeline_enable", "comet_timeline_dump", "comet_router_topk",
 )
 ROLES = ("load", "mma", "tmem_wait", "epilogue", "comm")
 
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_device_info": ([i32, _P32], i32),
         "comet_timeline_enable": ([vp, i32], i32),
         "comet_timeline_dump": ([vp, vp, c.c_size_t], i32),
+        "comet_router_topk": ([vp, i32, i32, i32, i32, i32, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -23,6 +23,8 @@ __global__ void moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const
 __global__ void combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb, const uint32_t* cb_flag,
                                       const int32_t* experts);
 __global__ void signal_x_ready_kernel(uint32_t* const* x_ready_peer, int rank, int world, uint32_t epoch);
+cudaError_t router_topk_launch(const void* logits, int logits_dtype, int M, int E, int topk, int norm,
+                               int32_t* experts, float* weights, int n_sm, cudaStream_t stream);
 __global__ void dispatch_local_kernel(const int32_t* gather_row, const int32_t* meta, const __nv_bfloat16* xs,
                                       __nv_bfloat16* xg, int n_embed, int M, int world, int rank);
 __global__ void combine_local_kernel(const int32_t* tok_pos, const float* combine_w, const __nv_bfloat16* yrows,
@@ -173,6 +175,26 @@ int comet_device_info(int device, int32_t out[4]) {
   out[1] = clusters;
   out[2] = major * 10 + minor;
   out[3] = (int)kLayerSmem;
+  return COMET_OK;
+}
+
+int comet_router_topk(const void* d_logits, int logits_dtype, int M, int E, int topk, int norm,
+                      int32_t* d_experts, float* d_weights, void* stream) {
+  if (M < 0 || E < 1 || E > 512) return fail(COMET_EINVAL, "router: need M >= 0 and 1 <= E <= 512 (M=%d, E=%d)", M, E);
+  if (topk < 1 || topk > E || topk > 32)
+    return fail(COMET_EINVAL, "router: topk=%d must be in [1, min(E=%d, 32)]", topk, E);
+  if (logits_dtype != 0 && logits_dtype != 1) return fail(COMET_EINVAL, "router: logits_dtype %d (0 fp32, 1 bf16)", logits_dtype);
+  if (norm < 0 || norm > 2) return fail(COMET_EINVAL, "router: norm %d (0 none, 1 top-k softmax, 2 full softmax)", norm);
+  if (norm != 0 && d_weights == nullptr) return fail(COMET_EINVAL, "router: norm %d needs a weights buffer", norm);
+  if (M > 0 && (d_logits == nullptr || d_experts == nullptr)) return fail(COMET_EINVAL, "router: null buffer");
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  CK(router_topk_launch(d_logits, logits_dtype, M, E, topk, norm, d_experts, norm ? d_weights : nullptr, n_sm,
+                        static_cast<cudaStream_t>(stream)));
   return COMET_OK;
 }
 

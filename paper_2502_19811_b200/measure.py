@@ -1,0 +1,191 @@
+"""Measured layer timings and the §8(d) roofline for any (model, EP x TP).
+
+``roofline`` restates SURVEY.md §8(d) / BASELINE.md for one routing:
+
+    FLOPs_r  = 4 * rows_r * N * K/tp            (two expert GEMMs, 2 flop / MAC)
+    Bytes_r  = 2 * N * (D_out_r + D_in_r)       bf16 bytes rank r transmits: dispatch
+                                                rows it sends + partial rows it pushes back
+    T        = max(max_r FLOPs_r / peak_flops, max_r Bytes_r / 900 GB/s)
+
+where rows_r are the (token, expert) rows hosted on r (routing.py:78-84
+counts over r's experts, replicated over the TP group) and D are distinct
+(token, remote destination rank) pairs (the dedup of the token-slot buffer,
+config.py:218-226).
+
+``EmulatedGroup`` runs every rank of a ``ParallelSpec`` on ONE GPU (their
+symmetric heaps linked in-process, NVLink traffic becomes HBM traffic) and
+times each rank's kernels with CUDA events on the launching stream; a rank's
+latency is the sum of its kernel times (index build + layer0 + layer1 +
+remote-combine finish) while it has the GPU to itself, and the group latency
+is the max over ranks -- the per-GPU time of a real EP deployment minus the
+NVLink/HBM bandwidth difference of the dispatched rows (<= 30 MB per rank at
+Mixtral EP=8, overlapped by the comm CTAs).
+"""
+
+from __future__ import annotations
+
+import math
+import statistics
+from dataclasses import dataclass
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from .config import ModelConfig, ParallelSpec
+from .routing import RoutingTable
+
+NVLINK_GBS = 900.0  # NVLink 5, per direction per GPU
+
+
+def rows_per_rank(routing: RoutingTable) -> np.ndarray:
+    """(token, expert) rows hosted on each rank (TP ranks of a group host the
+    same rows)."""
+    par, model = routing.parallel, routing.model
+    counts = np.asarray(routing.expert_counts, dtype=np.int64)
+    e_per = model.E // par.ep
+    per_group = counts.reshape(par.ep, e_per).sum(1)
+    return np.repeat(per_group, par.tp)
+
+
+def distinct_remote_pairs(routing: RoutingTable):
+    """(D_out[r], D_in[r]): distinct (token, remote destination rank) pairs
+    each rank sends / receives in the dispatch (every TP rank of a token's EP
+    groups is a destination, routing.py:106-117)."""
+    par, model = routing.parallel, routing.model
+    W, M = par.world_size, routing.workload.M
+    ex = routing.as_array().astype(np.int64)
+    d_out = np.zeros(W, np.int64)
+    d_in = np.zeros(W, np.int64)
+    if M == 0:
+        return d_out, d_in
+    e_per = model.E // par.ep
+    base = M // W
+    t = np.arange(M)
+    src = np.minimum(t // base, W - 1) if base > 0 else np.full(M, W - 1)
+    groups = ex // e_per                                   # [M, topk]
+    mask = np.zeros((M, par.ep), bool)
+    mask[np.repeat(t, ex.shape[1]), groups.reshape(-1)] = True
+    for g in range(par.ep):
+        for s in range(par.tp):
+            d = g * par.tp + s
+            sel = mask[:, g] & (src != d)
+            d_in[d] += int(sel.sum())
+            np.add.at(d_out, src[sel], 1)
+    return d_out, d_in
+
+
+@dataclass
+class Roofline:
+    flops_max: float       # max_r FLOPs_r
+    bytes_max: float       # max_r Bytes_r (per direction)
+    t_flops_ms: float
+    t_nvlink_ms: float
+    ms: float
+    bound: str
+    peak_tflops: float
+
+
+def roofline(routing: RoutingTable, peak_tflops: float, nvlink_gbs: float = NVLINK_GBS) -> Roofline:
+    model, par = routing.model, routing.parallel
+    rows = rows_per_rank(routing)
+    flops = 4.0 * rows.astype(np.float64) * model.N * (model.K // par.tp)
+    d_out, d_in = distinct_remote_pairs(routing)
+    byts = 2.0 * model.N * (d_out + d_in).astype(np.float64)
+    tf = float(flops.max()) / (peak_tflops * 1e12) * 1e3
+    tn = float(byts.max()) / (nvlink_gbs * 1e9) * 1e3
+    return Roofline(float(flops.max()), float(byts.max()), tf, tn, max(tf, tn),
+                    "tensor" if tf >= tn else "nvlink", peak_tflops)
+
+
+class EmulatedGroup:
+    """Every rank of ``parallel`` on one GPU, random-init bf16 weights per rank
+    (N(0,1)/sqrt(N), generated on the device), synthetic tokens."""
+
+    def __init__(self, model: ModelConfig, parallel: ParallelSpec, routing: RoutingTable, knobs=None,
+                 activation=None, seed: int = 0):
+        from . import _lib
+        from .executor import LayerKnobs, MoELayer, RankWeights, _ceil
+        torch = _lib.require_device()
+        self.torch, self.model, self.parallel, self.routing = torch, model, parallel, routing
+        self.M = M = routing.workload.M
+        W = parallel.world_size
+        e_per, kl = model.E // parallel.ep, model.K // parallel.tp
+        n_pad, k_pad = _ceil(model.N, 64), _ceil(kl, 64)
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        s = 1.0 / math.sqrt(model.N)
+        self.layers = []
+        for r in range(W):
+            w0t = torch.zeros(e_per, k_pad, n_pad, dtype=torch.bfloat16, device="cuda")
+            w1t = torch.zeros(e_per, n_pad, k_pad, dtype=torch.bfloat16, device="cuda")
+            for e in range(e_per):
+                w0t[e, :kl, :model.N] = (torch.randn(kl, model.N, device="cuda", generator=g) * s).to(torch.bfloat16)
+                w1t[e, :model.N, :kl] = (torch.randn(model.N, kl, device="cuda", generator=g) * s).to(torch.bfloat16)
+            self.layers.append(MoELayer(model, parallel, r, max(1, M), RankWeights(w0t, w1t),
+                                        activation=activation, knobs=knobs or LayerKnobs()))
+        if W > 1:
+            _lib.Context.link_local([l.ctx for l in self.layers])
+        x = torch.randn(M, model.N, device="cuda", generator=g).to(torch.bfloat16)
+        self.ex = torch.from_numpy(routing.as_array().copy()).cuda()
+        self.ys = []
+        for l in self.layers:
+            lo, hi = l.token_range(M)
+            l.place_tokens(x[lo:hi], M)
+            self.ys.append(torch.empty(hi - lo, n_pad, dtype=torch.bfloat16, device="cuda"))
+
+    def set_knobs(self, knobs) -> None:
+        for l in self.layers:
+            l.knobs = knobs
+
+    def _forward_timed(self, record: bool):
+        """One forward, phase-ordered over the emulated ranks (ranks share a
+        device, so each in-kernel wait is on work enqueued before it)."""
+        from .executor import index_flags
+        torch = self.torch
+        W = self.parallel.world_size
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if record else (lambda: None)
+        rec = {k: [] for k in ("index", "layer0", "layer1", "finish")}
+
+        def timed(key, fn):
+            a, b = ev(), ev()
+            if a is not None:
+                a.record()
+            fn()
+            if b is not None:
+                b.record()
+            rec[key].append((a, b))
+
+        for l in self.layers:
+            timed("index", lambda l=l: l.ctx.index_build(self.ex, self.M, flags=index_flags(W, l.n_comm1())))
+        for l in self.layers:
+            k = l.knobs
+            timed("layer0", lambda l=l, k=k: l.ctx.layer0(l.weights.w0t, l.act, k.n_comm0 if W > 1 else 0, k.group0))
+        for l, y in zip(self.layers, self.ys):
+            timed("layer1", lambda l=l, y=y: l.ctx.layer1(l.weights.w1t, None, y, l.n_comm1(), l.knobs.wave1))
+        for l, y in zip(self.layers, self.ys):
+            timed("finish", lambda l=l, y=y: l.ctx.combine_finish(y))
+        return rec
+
+    def measure(self, iters: int = 10, warmup: int = 3) -> Dict[str, object]:
+        """Median over ``iters`` forwards of each rank's kernel times (ms);
+        ``latency_ms`` = max over ranks of the per-rank sum."""
+        torch = self.torch
+        for _ in range(warmup):
+            self._forward_timed(False)
+        torch.cuda.synchronize()
+        per_iter = []
+        for _ in range(iters):
+            rec = self._forward_timed(True)
+            torch.cuda.synchronize()
+            per_iter.append({k: [a.elapsed_time(b) for a, b in v] for k, v in rec.items()})
+        W = self.parallel.world_size
+        med = {k: [statistics.median(it[k][r] for it in per_iter) for r in range(W)] for k in per_iter[0]}
+        per_rank = [sum(med[k][r] for k in med) for r in range(W)]
+        hot = int(np.argmax(per_rank))
+        return {"latency_ms": max(per_rank), "hot_rank": hot, "per_rank_ms": per_rank,
+                "kernels_ms_hot_rank": {k: med[k][hot] for k in med},
+                "kernels_ms_max": {k: max(med[k]) for k in med}}
+
+    def close(self) -> None:
+        for l in self.layers:
+            l.close()
+        self.layers = []

@@ -1,0 +1,115 @@
+"""Measurement matrix of SURVEY.md §8(d) on one B200.
+
+Every configuration runs the full fused forward with all EP x TP ranks
+emulated on this GPU (paper_2502_19811_b200.measure.EmulatedGroup): latency =
+max over ranks of the rank's kernel-time sum.  EP=1 rows are real
+single-GPU forwards and also time the unfused cuBLAS grouped-GEMM path.
+Roofline per §8(d) at the measured burst and sustained bf16 peaks.
+
+    python tools/matrix.py [--quick] [--out gpurun_out/matrix.jsonl]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from bench import load_peaks  # noqa: E402
+from paper_2502_19811_b200 import LayerKnobs, ModelConfig, ParallelSpec, WorkloadSpec, build_routing  # noqa: E402
+from paper_2502_19811_b200.measure import EmulatedGroup, roofline  # noqa: E402
+
+SHAPES = {"MX": (8, 2, 4096, 14336), "PH": (16, 2, 4096, 6400), "QW": (64, 8, 3584, 2560)}
+
+
+def configs(quick):
+    out = [("MX", 1, 1, 8192, 0.0), ("MX", 8, 1, 8192, 0.0), ("MX", 4, 1, 8192, 0.0), ("MX", 2, 1, 8192, 0.0),
+           ("MX", 8, 1, 8192, 0.032), ("MX", 8, 1, 8192, 0.05), ("PH", 4, 2, 8192, 0.0), ("QW", 8, 1, 8192, 0.0),
+           ("QW", 8, 1, 8192, 0.032), ("PH", 1, 1, 8192, 0.0), ("QW", 1, 1, 8192, 0.0)]
+    if not quick:
+        for ep in (1, 2, 4, 8):
+            for std in (0.0, 0.032):
+                for M in (1024, 2048, 4096, 8192, 16384, 32768):
+                    c = ("MX", ep, 1, M, std)
+                    if c not in out:
+                        out.append(c)
+    return out
+
+
+def unfused_ms(grp, iters=10):
+    from paper_2502_19811_b200.unfused import UnfusedLayer
+    l = grp.layers[0]
+    m = grp.model
+    kl = m.K
+    ul = UnfusedLayer(m, grp.parallel, 0, l.weights.w0t[:, :kl, :m.N].transpose(1, 2).contiguous(),
+                      l.weights.w1t[:, :m.N, :kl].transpose(1, 2).contiguous())
+    x = l.ctx.token_buffer()[:grp.M, :m.N]
+    for _ in range(3):
+        ul.forward(x, grp.ex, M=grp.M)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        ul.forward(x, grp.ex, M=grp.M)
+    e.record()
+    torch.cuda.synchronize()
+    del ul
+    return s.elapsed_time(e) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "matrix.jsonl"))
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--nc0", default="2,4,8", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
+    a = ap.parse_args()
+    burst, sust, _, src = load_peaks()
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as fh:
+        for shape, ep, tp, M, std in configs(a.quick):
+            E, topk, N, K = SHAPES[shape]
+            model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
+            par = ParallelSpec(tp=tp, ep=ep)
+            routing = build_routing(model, par, WorkloadSpec(M=M, seed=0, std=std))
+            rf_b, rf_s = roofline(routing, burst), roofline(routing, sust)
+            t0 = time.time()
+            grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=2, n_comm1=0))
+            best = None
+            for nc0 in ([0] if par.world_size == 1 else [int(v) for v in a.nc0.split(",")]):
+                grp.set_knobs(LayerKnobs(n_comm0=nc0, n_comm1=0))
+                r = grp.measure(iters=a.iters)
+                r["n_comm0"] = nc0
+                if best is None or r["latency_ms"] < best["latency_ms"]:
+                    best = r
+            rec = {"shape": shape, "E": E, "topk": topk, "N": N, "K": K, "ep": ep, "tp": tp, "M": M, "std": std,
+                   "emulated": par.world_size > 1, "latency_ms": round(best["latency_ms"], 4),
+                   "hot_rank": best["hot_rank"], "n_comm0": best["n_comm0"],
+                   "kernels_ms_hot_rank": {k: round(v, 4) for k, v in best["kernels_ms_hot_rank"].items()},
+                   "roofline_ms_burst": round(rf_b.ms, 4), "roofline_ms_sustained": round(rf_s.ms, 4),
+                   "roofline_bound": rf_b.bound, "t_nvlink_ms": round(rf_b.t_nvlink_ms, 4),
+                   "pct_roofline_burst": round(100 * rf_b.ms / best["latency_ms"], 1),
+                   "pct_roofline_sustained": round(100 * rf_s.ms / best["latency_ms"], 1),
+                   "peaks": {"burst_tflops": burst, "sustained_tflops": sust, "source": src}}
+            if par.world_size == 1:
+                try:
+                    u = unfused_ms(grp)
+                    rec["unfused_ms"] = round(u, 4)
+                    rec["speedup_vs_unfused"] = round(u / best["latency_ms"], 3)
+                except Exception as exc:  # report, keep going
+                    rec["unfused_error"] = repr(exc)[:200]
+            grp.close()
+            del grp
+            torch.cuda.empty_cache()
+            rec["wall_s"] = round(time.time() - t0, 1)
+            print(json.dumps(rec), flush=True)
+            fh.write(json.dumps(rec) + "\n")
+            fh.flush()
+
+
+if __name__ == "__main__":
+    main()
