@@ -128,6 +128,15 @@ int comet_layer0(comet_ctx* ctx, const void* w0t, int activation, int n_comm, in
 int comet_layer1(comet_ctx* ctx, const void* w1t, const float* combine_w, void* y_local, int n_comm,
                  int wave, void* stream);
 
+/* layer0 + layer1 in ONE persistent launch (what comet_forward runs): the
+ * same work as comet_layer0 then comet_layer1 (n_comm1 = 0), with layer1
+ * units claimed as soon as the layer0 H rows of their 256-row pair are
+ * complete, and the dispatch CTAs joining the GEMMs once their rows are
+ * pulled -- the paper's overlap carried across the layer boundary
+ * (executor.py:200-217 runs the two loops back to back). */
+int comet_layers(comet_ctx* ctx, const void* w0t, const void* w1t, const float* combine_w, void* y_local,
+                 int activation, int n_comm0, int group0, int wave1, void* stream);
+
 /* Remote half of the combine (world > 1): wait for every sender's partial
  * rows of this rank's tokens and sum them in ascending rank order
  * (executor.py:239-245).  Separate from comet_layer1 so that ranks emulated

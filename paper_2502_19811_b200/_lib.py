@@ -30,7 +30,7 @@ EXPORTS = (
     "comet_last_error", "comet_version", "comet_ctx_create", "comet_ctx_destroy",
     "comet_symm_export", "comet_symm_import", "comet_link_local", "comet_token_buffer",
     "comet_routing_buffer", "comet_index_build", "comet_index_build_ex", "comet_index_sizes", "comet_index_download",
-    "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_combine_finish", "comet_forward",
+    "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_layers", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
     "comet_timeline_enable", "comet_timeline_dump", "comet_router_topk",
 )
@@ -94,6 +94,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_layer0": ([vp, vp, i32, i32, i32, vp], i32),
         "comet_layer1": ([vp, vp, vp, vp, i32, i32, vp], i32),
         "comet_combine_finish": ([vp, vp, vp], i32),
+        "comet_layers": ([vp, vp, vp, vp, vp, i32, i32, i32, i32, vp], i32),
         "comet_forward": ([vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp], i32),
         "comet_device_info": ([i32, _P32], i32),
         "comet_timeline_enable": ([vp, i32], i32),
@@ -273,6 +274,14 @@ class Context:
         cw = ctypes.c_void_p(combine_w.data_ptr()) if combine_w is not None else None
         check(self.lib.comet_layer1(self.handle, ctypes.c_void_p(w1t.data_ptr()), cw,
                                     ctypes.c_void_p(y_local.data_ptr()), n_comm, wave,
+                                    ctypes.c_void_p(self._stream(stream))))
+
+    def layers(self, w0t, w1t, combine_w, y_local, activation: int = 0, n_comm0: int = 2, group0: int = 4,
+               wave1: int = 4, stream=None) -> None:
+        """layer0 + layer1 in one persistent launch (comet_layers)."""
+        cw = ctypes.c_void_p(combine_w.data_ptr()) if combine_w is not None else None
+        check(self.lib.comet_layers(self.handle, ctypes.c_void_p(w0t.data_ptr()), ctypes.c_void_p(w1t.data_ptr()),
+                                    cw, ctypes.c_void_p(y_local.data_ptr()), activation, n_comm0, group0, wave1,
                                     ctypes.c_void_p(self._stream(stream))))
 
     def timeline_enable(self, cap: int) -> None:

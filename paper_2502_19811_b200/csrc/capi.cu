@@ -18,8 +18,9 @@
 
 namespace comet {
 __global__ void index_build_kernel(IndexDev ix);
-__global__ void moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                                 const __grid_constant__ CUtensorMap tm_out, const LayerArgs p);
+__global__ void moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_b0,
+                                 const __grid_constant__ CUtensorMap tm_a1, const __grid_constant__ CUtensorMap tm_b1,
+                                 const __grid_constant__ KernelArgs f);
 __global__ void combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb, const uint32_t* cb_flag,
                                       const int32_t* experts);
 __global__ void signal_x_ready_kernel(uint32_t* const* x_ready_peer, int rank, int world, uint32_t epoch);
@@ -144,6 +145,9 @@ struct comet_ctx {
   void* last_y = nullptr;
   const float* last_combine_w = nullptr;
   MapCache w0c, w1c;
+  uint32_t* sched = nullptr;  // [2] unit claim / CTA exit counters of the layer kernel (self-resetting)
+  uint32_t* h_cnt = nullptr;  // [cap_rows_pad / 128 + 1] fused-launch H tile counters (self-resetting)
+  int n_h = 0;
 };
 
 extern "C" {
@@ -185,7 +189,7 @@ int comet_router_topk(const void* d_logits, int logits_dtype, int M, int E, int 
     return fail(COMET_EINVAL, "router: topk=%d must be in [1, min(E=%d, 32)]", topk, E);
   if (logits_dtype != 0 && logits_dtype != 1) return fail(COMET_EINVAL, "router: logits_dtype %d (0 fp32, 1 bf16)", logits_dtype);
   if (norm < 0 || norm > 2) return fail(COMET_EINVAL, "router: norm %d (0 none, 1 top-k softmax, 2 full softmax)", norm);
-  if (norm != 0 && d_weights == nullptr) return fail(COMET_EINVAL, "router: norm %d needs a weights buffer", norm);
+  if (M > 0 && norm != 0 && d_weights == nullptr) return fail(COMET_EINVAL, "router: norm %d needs a weights buffer", norm);
   if (M > 0 && (d_logits == nullptr || d_experts == nullptr)) return fail(COMET_EINVAL, "router: null buffer");
   static int n_sm = 0;
   if (n_sm == 0) {
@@ -328,6 +332,8 @@ int comet_ctx_destroy(comet_ctx* x) {
   cudaFree(x->xg);
   cudaFree(x->xg_ready);
   cudaFree(x->tile_done);
+  cudaFree(x->sched);
+  cudaFree(x->h_cnt);
   cudaFree(x->timeline);
   cudaFree(x->counters);
   cudaFree(x->routing);
@@ -544,11 +550,16 @@ static int ensure_work(comet_ctx* x) {
   CK(cudaMalloc(&x->H, (size_t)x->cap_rows_pad * x->k_local * 2));
   CK(cudaMalloc(&x->yrows, (size_t)x->cap_rows_pad * c.N * 2));
   CK(cudaMalloc(&x->xg, (size_t)x->cap_rows_pad * c.N * 2));
-  CK(cudaMalloc(&x->xg_ready, sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
-  CK(cudaMemset(x->xg_ready, 0, sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
-  const size_t td = sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1) * x->nb1;
+  CK(cudaMalloc(&x->xg_ready, 2 * sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
+  CK(cudaMemset(x->xg_ready, 0, 2 * sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1)));
+  const size_t td = sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1) * x->nb1 * 2;
   CK(cudaMalloc(&x->tile_done, td));
   CK(cudaMemset(x->tile_done, 0, td));
+  x->n_h = x->cap_rows_pad / kTileRows + 1;
+  CK(cudaMalloc(&x->sched, sizeof(uint32_t) * 2));
+  CK(cudaMemset(x->sched, 0, sizeof(uint32_t) * 2));
+  CK(cudaMalloc(&x->h_cnt, sizeof(uint32_t) * x->n_h));
+  CK(cudaMemset(x->h_cnt, 0, sizeof(uint32_t) * x->n_h));
   int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
   if (!rc) rc = make_map(&x->tm_xg, x->xg, x->cap_rows_pad, c.N, 128);
   if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
@@ -586,6 +597,7 @@ static LayerArgs base_args(comet_ctx* x) {
   a.n_local = x->ix.n_local;
   a.xg = x->xg;
   a.xg_ready = x->xg_ready;
+  a.xg_cnt = x->xg_ready + (x->cap_rows_pad / kTileRows + 1);
   a.pull_token = x->ix.pull_token;
   a.pull_src = x->ix.pull_src;
   a.tok_pos = x->ix.tok_pos;
@@ -608,16 +620,24 @@ static LayerArgs base_args(comet_ctx* x) {
   return a;
 }
 
-static int launch_layer(comet_ctx* x, const LayerArgs& a, const CUtensorMap& ta, const CUtensorMap& tb,
-                        const CUtensorMap& to, int n_comm, cudaStream_t st) {
-  if (n_comm < 0 || (n_comm & 1)) return fail(COMET_EINVAL, "n_comm=%d must be even and >= 0", n_comm);
+static int layer_grid(comet_ctx* x) {
   int grid = std::min(x->n_sm, 2 * x->max_clusters);
   if (const char* e = getenv("COMET_GRID")) grid = std::min(grid, atoi(e));
-  LayerArgs b = a;
-  b.n_compute = grid - n_comm;
-  if (b.n_compute < 2) return fail(COMET_EINVAL, "n_comm=%d leaves no compute pair (grid %d)", n_comm, grid);
+  return grid & ~1;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static int launch_kernel(comet_ctx* x, KernelArgs& f, const CUtensorMap& a0, const CUtensorMap& b0,
+                         const CUtensorMap& a1, const CUtensorMap& b1, cudaStream_t st) {
+  f.sched = x->sched;
+  f.h_cnt = x->h_cnt;
+  f.n_h = x->n_h;
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(grid);
+  lc.gridDim = dim3(layer_grid(x));
   lc.blockDim = dim3(kLayerThreads);
   lc.dynamicSmemBytes = kLayerSmem;
   lc.stream = st;
@@ -628,47 +648,46 @@ static int launch_layer(comet_ctx* x, const LayerArgs& a, const CUtensorMap& ta,
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, ta, tb, to, b));
+  CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, a0, b0, a1, b1, f));
   return COMET_OK;
 }
 
-int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int group, void* stream) {
+// Layer0 arguments (dispatch + FC1 + activation); n_comm dispatch CTAs.
+static int layer0_args(comet_ctx* x, const void* w0t, int activation, int n_comm, int group, LayerArgs* out) {
   const auto& c = x->cfg;
   if (activation < 0 || activation > COMET_ACT_TANH) return fail(COMET_EINVAL, "bad activation %d", activation);
   if (group < 1) return fail(COMET_EINVAL, "group must be >= 1");
   if (c.world > 1 && n_comm < 2) return fail(COMET_EINVAL, "world > 1: layer0 needs n_comm >= 2 (NVLink dispatch CTAs)");
   if (c.world == 1) n_comm = 0;  // no remote rows: every row is placed by the local dispatch
-  CK(cudaSetDevice(c.device));
+  if (n_comm < 0 || (n_comm & 1)) return fail(COMET_EINVAL, "n_comm=%d must be even and >= 0", n_comm);
+  const int grid = layer_grid(x);
+  if (grid - n_comm < 2) return fail(COMET_EINVAL, "n_comm=%d leaves no compute pair (grid %d)", n_comm, grid);
   if (int rc = ensure_work(x)) return rc;
   if (int rc = get_weight_map(x, x->w0c, w0t, (uint64_t)x->E_r * x->k_local, c.N)) return rc;
   LayerArgs a = base_args(x);
   a.layer = 0;
+  a.n_compute = grid - n_comm;
   a.n_blocks = x->nb0;
   a.k_blocks = x->kb0;
   a.b_rows = x->k_local;
   a.order_group = group;
+  a.raster = 0;
   a.activation = activation;
-  {
-    const char* sp = getenv("COMET_SPLIT");
-    a.split_tail = sp == nullptr || atoi(sp) != 0;
-  }
+  a.split_tail = env_int("COMET_SPLIT", 1) != 0;
+  a.chunk_rows = std::max(1, std::min(32, env_int("COMET_CHUNK", 16)));
   a.pairs = x->ix.pairs0;
   a.out = x->H;
   a.out_ld = x->k_local;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // HBM-local rows first (whole GPU, bandwidth-bound); comm CTAs pull only remote rows.
-  dispatch_local_kernel<<<x->n_sm * 4, 256, 0, st>>>(x->ix.gather_row, x->ix.meta, x->xs, x->xg, c.N, x->M, c.world,
-                                                     c.rank);
-  CK(cudaGetLastError());
-  return launch_layer(x, a, x->tm_xg, x->w0c.map, x->tm_H, n_comm, st);
+  *out = a;
+  return COMET_OK;
 }
 
-int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_local, int n_comm, int wave,
-                 void* stream) {
+// Layer1 arguments (FC2 + top-k combine); n_comm combine CTAs (world 1 only).
+static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, void* y_local, int n_comm, int wave,
+                       bool alone, LayerArgs* out) {
   const auto& c = x->cfg;
   if (wave < 1) return fail(COMET_EINVAL, "wave must be >= 1");
-  if (n_comm < 0) return fail(COMET_EINVAL, "n_comm=%d must be >= 0", n_comm);
-  CK(cudaSetDevice(c.device));
+  if (n_comm < 0 || (n_comm & 1)) return fail(COMET_EINVAL, "n_comm=%d must be even and >= 0", n_comm);
   if (int rc = ensure_work(x)) return rc;
   if (int rc = get_weight_map(x, x->w1c, w1t, (uint64_t)x->E_r * c.N, x->k_local)) return rc;
   LayerArgs a = base_args(x);
@@ -678,6 +697,7 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   a.b_rows = c.N;
   a.order_group = wave;
   a.order_group2 = 8;
+  a.raster = 1;
   a.pairs = x->ix.pairs1;
   a.out = x->yrows;
   a.out_ld = c.N;
@@ -689,19 +709,84 @@ int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_
   // without communication CTAs.  Otherwise combine CTAs (n_comm > 0) or the
   // local combine kernel reduce yrows.  At world 1 the fold's tile waits cost
   // what the local combine kernel saves (A/B in DESIGN.md), so it is opt-in.
-  const char* f1 = getenv("COMET_FUSE1");
-  a.fuse_combine = c.world > 1 || (n_comm == 0 && f1 != nullptr && atoi(f1) != 0);
+  a.fuse_combine = c.world > 1 || (n_comm == 0 && env_int("COMET_FUSE1", 0) != 0);
   a.tile_done = x->tile_done;
-  if (c.world > 1) n_comm = 0;
+  if (c.world > 1 || !alone) n_comm = 0;  // combine CTAs only in a layer1-alone launch at world 1
+  const int grid = layer_grid(x);
+  if (grid - n_comm < 2) return fail(COMET_EINVAL, "n_comm=%d leaves no compute pair (grid %d)", n_comm, grid);
+  a.n_compute = grid - n_comm;
+  // the last layer1 units may run as 256-column halves (finer tail; off by
+  // default: a half moves 64 B/cycle/SM for its MMAs instead of 48 and ran
+  // ~35% slower per FLOP, tools/fused_timeline.py)
+  a.split_units = env_int("COMET_SPLIT1", 0);
+  *out = a;
+  return COMET_OK;
+}
+
+static int local_combine(comet_ctx* x, const LayerArgs& a, const float* combine_w, void* y_local, cudaStream_t st) {
+  const auto& c = x->cfg;
+  if (a.n_compute < layer_grid(x) || a.fuse_combine) return COMET_OK;  // combine CTAs / epilogue did it
+  const int t0 = token_start_of(c.rank, x->M, c.world);
+  const int n_tok = token_stop_of(c.rank, x->M, c.world) - t0;
+  combine_local_kernel<<<x->n_sm * 8, 256, 0, st>>>(x->ix.tok_pos, combine_w, x->yrows,
+                                                    static_cast<__nv_bfloat16*>(y_local), t0, n_tok, c.topk, c.N);
+  CK(cudaGetLastError());
+  return COMET_OK;
+}
+
+static int dispatch_local(comet_ctx* x, cudaStream_t st) {
+  const auto& c = x->cfg;
+  // HBM-local rows first (whole GPU, bandwidth-bound); dispatch CTAs pull only remote rows.
+  dispatch_local_kernel<<<x->n_sm * 4, 256, 0, st>>>(x->ix.gather_row, x->ix.meta, x->xs, x->xg, c.N, x->M, c.world,
+                                                     c.rank);
+  CK(cudaGetLastError());
+  return COMET_OK;
+}
+
+int comet_layer0(comet_ctx* x, const void* w0t, int activation, int n_comm, int group, void* stream) {
+  CK(cudaSetDevice(x->cfg.device));
+  KernelArgs f{};
+  if (int rc = layer0_args(x, w0t, activation, n_comm, group, &f.l[0])) return rc;
+  f.mode = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (int rc = launch_layer(x, a, x->tm_H, x->w1c.map, x->tm_y, n_comm, st)) return rc;
-  if (n_comm == 0 && !a.fuse_combine) {
-    const int t0 = token_start_of(c.rank, x->M, c.world);
-    const int n_tok = token_stop_of(c.rank, x->M, c.world) - t0;
-    combine_local_kernel<<<x->n_sm * 8, 256, 0, st>>>(x->ix.tok_pos, combine_w, x->yrows,
-                                                      static_cast<__nv_bfloat16*>(y_local), t0, n_tok, c.topk, c.N);
-    CK(cudaGetLastError());
-  }
+  if (int rc = dispatch_local(x, st)) return rc;
+  return launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_xg, x->w0c.map, st);
+}
+
+int comet_layer1(comet_ctx* x, const void* w1t, const float* combine_w, void* y_local, int n_comm, int wave,
+                 void* stream) {
+  CK(cudaSetDevice(x->cfg.device));
+  KernelArgs f{};
+  if (int rc = layer1_args(x, w1t, combine_w, y_local, n_comm, wave, true, &f.l[1])) return rc;
+  f.mode = 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = launch_kernel(x, f, x->tm_H, x->w1c.map, x->tm_H, x->w1c.map, st)) return rc;
+  if (int rc = local_combine(x, f.l[1], combine_w, y_local, st)) return rc;
+  x->last_y = y_local;
+  x->last_combine_w = combine_w;
+  return COMET_OK;
+}
+
+int comet_layers(comet_ctx* x, const void* w0t, const void* w1t, const float* combine_w, void* y_local,
+                 int activation, int n_comm0, int group0, int wave1, void* stream) {
+  CK(cudaSetDevice(x->cfg.device));
+  KernelArgs f{};
+  if (int rc = layer0_args(x, w0t, activation, n_comm0, group0, &f.l[0])) return rc;
+  if (int rc = layer1_args(x, w1t, combine_w, y_local, 0, wave1, false, &f.l[1])) return rc;
+  f.mode = 2;
+  // layer1 in the layer0 pair groups (a group's layer1 units become ready
+  // together).  Without fold chains (no fused combine, or one hosted expert
+  // per token) layer1 walks the layer0 claim-ordered pair table itself, so
+  // its first group is the group layer0 finished first; with fold chains it
+  // keeps the expert-ascending table (a token's earlier hosted rows must sit
+  // in earlier units of the same columns).
+  f.l[1].raster = 2;
+  f.l[1].order_group2 = f.l[0].order_group;
+  if (!f.l[1].fuse_combine || x->E_r == 1 || x->cfg.topk == 1) f.l[1].pairs = x->ix.pairs0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = dispatch_local(x, st)) return rc;
+  if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
+  if (int rc = local_combine(x, f.l[1], combine_w, y_local, st)) return rc;
   x->last_y = y_local;
   x->last_combine_w = combine_w;
   return COMET_OK;
@@ -739,7 +824,10 @@ int comet_combine_finish(comet_ctx* x, void* y_local, void* stream) {
   a.layer = 1;
   a.n_blocks = x->nb1;
   a.y_local = static_cast<__nv_bfloat16*>(y_local ? y_local : x->last_y);
-  combine_finish_kernel<<<x->n_sm, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, x->cb, x->cb_flag,
+  const int n_own = token_stop_of(c.rank, x->M, c.world) - token_start_of(c.rank, x->M, c.world);
+  const int items = n_own * ((c.N / 8 + 127) / 128);  // one warp per (token, 1024-column segment)
+  const int blocks = std::max(1, std::min(x->n_sm * 8, (items + 7) / 8));
+  combine_finish_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, x->cb, x->cb_flag,
                                                                                x->ix.experts);
   CK(cudaGetLastError());
   return COMET_OK;
@@ -755,8 +843,15 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
   if (int rc = comet_index_build_ex(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), flags,
                                     stream))
     return rc;
-  if (int rc = comet_layer0(x, w0t, activation, n_comm0, group0, stream)) return rc;
-  if (int rc = comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream)) return rc;
+  // One launch for both layers (layer1 tiles start as their H rows land),
+  // unless world-1 combine CTAs are asked for or COMET_FUSED=0.
+  const bool fused = env_int("COMET_FUSED", 1) != 0 && !(x->cfg.world == 1 && n_comm1 > 0);
+  if (fused) {
+    if (int rc = comet_layers(x, w0t, w1t, combine_w, y_local, activation, n_comm0, group0, wave1, stream)) return rc;
+  } else {
+    if (int rc = comet_layer0(x, w0t, activation, n_comm0, group0, stream)) return rc;
+    if (int rc = comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream)) return rc;
+  }
   return comet_combine_finish(x, y_local, stream);
 }
 

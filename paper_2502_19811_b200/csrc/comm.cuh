@@ -17,8 +17,8 @@ namespace comm {
 constexpr int kMaxSlots = 224;
 constexpr int kReducers = 7;               // combine: warps 1..7
 constexpr int kBatch = 16;                 // jobs described per loader pass
-constexpr uint32_t kRingBytes = 160 * 1024;
-constexpr int kFreeLag = 8;                // dispatch: bulk-store groups before a slot is reused
+constexpr uint32_t kRingBytes = 192 * 1024;
+constexpr int kFreeLag = 2;                // dispatch: bulk-store groups before a slot is reused
 constexpr int kPubLag = 24;                // dispatch: groups in flight before a tile is published
 
 struct JobDesc {
@@ -30,7 +30,8 @@ struct CommSmem {
   uint64_t full[kMaxSlots];
   uint64_t empty[kMaxSlots];
   JobDesc desc[kMaxSlots];
-  int pub_tile[64];
+  int pub_tile[64];  // tile | rows << 16 of a pending dispatch chunk
+  int pub_rows[64];  // remote rows of that tile
   int pub_job[64];
   unsigned long long pub_t0[64];
   const __nv_bfloat16* xs_peer[kMaxWorld];
@@ -46,13 +47,14 @@ __device__ __forceinline__ void comm_record(const LayerArgs& p, int idx, int tas
 }
 
 // Layer1 (world > 1): one contributor finished its rows of column block nb --
-// a compute CTA's 128 epilogue-pushed rows of one unit, or a combine CTA's
-// reduced tokens.  The contributor completing the count (2 per pair unit + one
-// per combine CTA) publishes the block to every peer's combine flags.
-__device__ __forceinline__ void nb_contributed(const LayerArgs& p, int nb, uint32_t target) {
+// a compute CTA's 128 epilogue-pushed rows of one unit (2 per full unit, 1
+// per 256-column half unit), or a combine CTA's reduced tokens (1).  The
+// contributor completing the count (4 per pair + one per combine CTA)
+// publishes the block to every peer's combine flags.
+__device__ __forceinline__ void nb_contributed(const LayerArgs& p, int nb, uint32_t amount, uint32_t target) {
   ptx::fence_acq_rel_sys();
-  const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.nb_sent + nb, 1u);
-  if (prev + 1u == target) {
+  const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.nb_sent + nb, amount);
+  if (prev + amount == target) {
     ptx::fence_acq_rel_sys();
     for (int d = 0; d < p.world; ++d) ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * p.n_blocks + nb, p.epoch);
   }
@@ -96,10 +98,41 @@ __device__ __forceinline__ bool remote_rows(const LayerArgs& p, int q, int& padr
   return nr > 0;
 }
 
-// layer0 dispatch: fill the expert-sorted shared tensor xg tile by tile in the
-// compute schedule's claim order (locality-first, resolver.py:206-252): local
-// rows from this rank's token buffer, remote rows pulled over NVLink from the
-// source rank's token buffer; publish each 128-row tile with a ready epoch.
+// A dispatch CTA that finished joins the compute pairs: its smem becomes
+// stage buffers, so retire the ring barriers first (every bulk copy has
+// completed: the storer waited for all groups, the loads were all consumed).
+__device__ __forceinline__ void comm_release(const LayerArgs& p, uint8_t* smem) {
+  const uint32_t row_bytes = static_cast<uint32_t>(p.n_embed) * 2u;
+  const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / row_bytes));
+  CommSmem* cs = comm_smem(smem);
+  for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
+    ptx::mbar_inval(cs->full + i);
+    ptx::mbar_inval(cs->empty + i);
+  }
+}
+
+// Dispatch work items: chunks of chunk_rows (default 16) remote rows of one 128-row tile,
+// enumerated in the compute schedule's claim order (tile-major) and dealt
+// round-robin to the dispatch CTAs, so a tile's rows are pulled by several
+// CTAs at once.  fn(q, padrow0, r_begin, r_end, nr) for this CTA's items.
+template <class F>
+__device__ __forceinline__ void for_my_items(const LayerArgs& p, int cid, int n_comm, F&& fn) {
+  const int n_tiles = 2 * p.meta[kMetaPairs];
+  const int chunk = p.chunk_rows;  // 1..32
+  int item = 0;
+  for (int q = 0; q < n_tiles; ++q) {
+    int padrow0, nr;
+    if (!remote_rows(p, q, padrow0, nr)) continue;
+    for (int r0 = 0; r0 < nr; r0 += chunk, ++item)
+      if (item % n_comm == cid) fn(q, padrow0, r0, min(nr, r0 + chunk), nr);
+  }
+}
+
+// layer0 dispatch: fill the remote rows of the expert-sorted shared tensor xg
+// (local rows were placed by dispatch_local_kernel) in the compute schedule's
+// claim order (locality-first, resolver.py:206-252), pulling each row over
+// NVLink from its source rank's token buffer.  A tile is published (ready
+// epoch) by whichever CTA lands its last chunk (per-tile row counters).
 __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
   const uint32_t row_bytes = static_cast<uint32_t>(p.n_embed) * 2u;  // <= kRingBytes / 8 (host-checked)
   const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / row_bytes));
@@ -108,60 +141,59 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
   const int n_comm = gridDim.x - p.n_compute;
   const int cid = blockIdx.x - p.n_compute;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int P = p.meta[kMetaPairs];
-  const int n_tiles = 2 * P;
   if (warp == 0) {
-    // ---- loader warp: lane-parallel index loads for 32 rows, then lane 0
+    // ---- loader warp: lane-parallel index loads for a chunk, then lane 0
     // issues them in job order (slot waits never couple lanes of one batch) ----
     uint64_t ready_mask = 1ull << p.rank;
     int k = 0;
-    for (int q = cid; q < n_tiles; q += n_comm) {
-      int padrow0, nr;
-      if (!remote_rows(p, q, padrow0, nr)) continue;
-      for (int r0 = 0; r0 < nr; r0 += 32) {
-        const int r = r0 + lane;
-        const int t = r < nr ? p.gather_row[padrow0 + r] : 0;
-        const int src = src_rank_of(t, p.M, p.world);
-        const int nb = min(32, nr - r0);
-        for (int i = 0; i < nb; ++i) {
-          const int ti = __shfl_sync(0xffffffffu, t, i);
-          const int si = __shfl_sync(0xffffffffu, src, i);
-          if (lane == 0) {
-            if (!((ready_mask >> si) & 1)) {
-              while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
-              ready_mask |= 1ull << si;
-            }
-            const int job = k + i;
-            const int slot = job % n_slots;
-            ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
-            ptx::mbar_arrive_expect_tx(cs->full + slot, row_bytes);
-            ptx::bulk_load(smem + slot * row_bytes, cs->xs_peer[si] + static_cast<long long>(ti) * p.n_embed,
-                           row_bytes, cs->full + slot);
+    for_my_items(p, cid, n_comm, [&](int q, int padrow0, int rb, int re, int nr) {
+      const int n = re - rb;
+      const int t = lane < n ? p.gather_row[padrow0 + rb + lane] : 0;
+      const int src = src_rank_of(t, p.M, p.world);
+      for (int i = 0; i < n; ++i) {
+        const int ti = __shfl_sync(0xffffffffu, t, i);
+        const int si = __shfl_sync(0xffffffffu, src, i);
+        if (lane == 0) {
+          if (!((ready_mask >> si) & 1)) {
+            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
+            ready_mask |= 1ull << si;
           }
+          const int job = k + i;
+          const int slot = job % n_slots;
+          ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(cs->full + slot, row_bytes);
+          ptx::bulk_load(smem + slot * row_bytes, cs->xs_peer[si] + static_cast<long long>(ti) * p.n_embed,
+                         row_bytes, cs->full + slot);
         }
-        k += nb;
-        __syncwarp();
       }
-    }
+      k += n;
+      __syncwarp();
+    });
   } else if (warp == 1 && lane == 0) {
-    // ---- storer: slot -> xg row; publish tiles once their writes landed ----
+    // ---- storer: slot -> xg row; count each chunk once its writes landed ----
     int k = 0, head = 0, tail = 0, n_rec = 0;
     auto publish_upto = [&](int done_job) {
       while (head != tail && cs->pub_job[head & 63] <= done_job) {
+        const int e = head & 63;
+        const int q = cs->pub_tile[e] & 0xFFFF, rows = cs->pub_tile[e] >> 16;
+        const int nr = cs->pub_rows[e];
         ptx::fence_async_global();
-        // end stamp taken before the release: a consumer that observes the
-        // flag always stamps a later time (measured dependency audit)
-        const unsigned long long t_pub = ptx::globaltimer();
-        ptx::st_release_gpu(p.xg_ready + cs->pub_tile[head & 63], p.epoch);
-        comm_record(p, n_rec++, cs->pub_tile[head & 63], cs->pub_t0[head & 63], t_pub);
+        // end stamp taken before the count / release: a consumer that observes
+        // the tile's flag always stamps a later time (measured dependency audit)
+        const unsigned long long t_done = ptx::globaltimer();
+        comm_record(p, n_rec++, q, cs->pub_t0[e], t_done);
+        const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.xg_cnt + q, static_cast<uint32_t>(rows));
+        if (prev + static_cast<uint32_t>(rows) == static_cast<uint32_t>(nr)) {
+          // last chunk of tile q: every CTA's rows are visible (acq_rel chain)
+          p.xg_cnt[q] = 0u;  // no other access this launch; ready for the next
+          ptx::st_release_gpu(p.xg_ready + q, p.epoch);
+        }
         ++head;
       }
     };
-    for (int q = cid; q < n_tiles; q += n_comm) {
-      int padrow0, nr;
-      if (!remote_rows(p, q, padrow0, nr)) continue;
-      const unsigned long long t_tile = ptx::globaltimer();
-      for (int r = 0; r < nr; ++r, ++k) {
+    for_my_items(p, cid, n_comm, [&](int q, int padrow0, int rb, int re, int nr) {
+      const unsigned long long t_item = ptx::globaltimer();
+      for (int r = rb; r < re; ++r, ++k) {
         const int slot = k % n_slots;
         ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
         ptx::bulk_store(p.xg + static_cast<long long>(padrow0 + r) * p.n_embed, smem + slot * row_bytes, row_bytes);
@@ -173,15 +205,17 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
           publish_upto(k - kPubLag);
         }
       }
-      cs->pub_tile[tail & 63] = q;
-      cs->pub_job[tail & 63] = k - 1;
-      cs->pub_t0[tail & 63] = t_tile;
+      const int e = tail & 63;
+      cs->pub_tile[e] = q | ((re - rb) << 16);
+      cs->pub_rows[e] = nr;
+      cs->pub_job[e] = k - 1;
+      cs->pub_t0[e] = t_item;
       ++tail;
       if (tail - head >= 60) {
         ptx::bulk_wait<0>();
         publish_upto(k);
       }
-    }
+    });
     ptx::bulk_wait<0>();
     publish_upto(k);
   }
@@ -203,7 +237,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = p.meta[kMetaPairs];
   const int n_tok = p.meta[kMetaCombineTok];
-  const uint32_t target = 2u * static_cast<uint32_t>(P);
+  const uint32_t target = 4u * static_cast<uint32_t>(P);  // nb_done counts 256-column halves per CTA
   const int start_r = token_start_of(p.rank, p.M, p.world);
   const int jobs = n_tok > cid ? (n_tok - cid + n_comm - 1) / n_comm : 0;  // tokens of this CTA per nb
   if (warp == 0) {
@@ -299,7 +333,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
       // all reducers of this CTA finished nb -> count the CTA; last CTA signals peers
       __threadfence_system();
       ptx::named_bar_sync(2, kReducers * 32);
-      if (threadIdx.x == 32) nb_contributed(p, nb, target + static_cast<uint32_t>(n_comm));
+      if (threadIdx.x == 32) nb_contributed(p, nb, 1u, target + static_cast<uint32_t>(n_comm));
     }
   }
 }

@@ -25,9 +25,11 @@ struct LayerArgs {
   int k_blocks;           // 64-wide contraction blocks
   int b_rows;             // weight rows per expert in the 2D B view
   int order_group;        // layer0: pairs per group; layer1: n-blocks per wave
-  int order_group2;       // layer1: pairs per group inside a wave
+  int order_group2;       // layer1: pairs per group inside a wave (raster 1) / per outer group (raster 2)
+  int raster;             // unit order: 0 layer0 groups, 1 layer1 waves, 2 pair groups then waves (fused)
   int activation;
-  int split_tail;         // layer0: cut a mostly idle last round into 256-column half units
+  int split_tail;         // layer0 (alone): cut a mostly idle last round into 256-column half units
+  int split_units;        // layer1: the last `split_units` full units run as 256-column halves
   uint32_t epoch;
   int debug;              // bit0: comm CTAs idle; bit1: layer0 A by 2D tile (no gather); bit2: spin waits
 
@@ -39,6 +41,8 @@ struct LayerArgs {
   const int32_t* n_local;     // [E_r] local (prefix) rows of each hosted expert
   __nv_bfloat16* xg;          // [Rpad_cap, N] layer0 A: dispatched rows, expert-sorted
   uint32_t* xg_ready;         // [Rpad_cap / 128] epoch when a 128-row tile of xg is filled
+  uint32_t* xg_cnt;           // [Rpad_cap / 128] remote rows landed per tile (reset by its publisher)
+  int chunk_rows;             // layer0 dispatch work item: rows of one tile (1..32)
   const int32_t* pull_token;  // layer0 comm
   const int32_t* pull_src;
   const int32_t* tok_pos;     // [M*topk]
@@ -47,7 +51,8 @@ struct LayerArgs {
   const int32_t* row_widx;    // [Rpad] t * topk + slot of each padded row
   int fuse_combine;           // layer1: the epilogue of each token's last hosted row folds the
                               // earlier rows in and writes y (world 1) / pushes to the source rank
-  uint32_t* tile_done;        // [Rpad/128 * n_blocks] epoch when a 128-row tile's yrows of an n-block landed
+  uint32_t* tile_done;        // [Rpad/128 * n_blocks * 2] epoch when a 128-row tile's yrows of a 256-column
+                              // half of an n-block landed
   const float* combine_w;     // [M*topk] or null
 
   // buffers
@@ -69,6 +74,22 @@ struct LayerArgs {
   // at ((c * kRoles + k) * timeline_cap + r) * 2 as {start_ns, end_ns | tag}
   unsigned long long* timeline;
   int timeline_cap;
+};
+
+// One launch of the persistent layer kernel.  mode 0: layer0 alone; mode 1:
+// layer1 alone; mode 2: layer0 then layer1 in ONE launch -- a layer1 unit
+// starts as soon as the layer0 H rows of its 256-row pair are complete (per
+// 128-row tile counters), so layer0's last round overlaps layer1's first.
+// Work units are claimed dynamically (one atomic per unit, in sequence
+// order): layer0 units, then layer1 units.  Dispatch CTAs (layer0 comm,
+// [l[0].n_compute, grid)) join the compute pairs once their rows are pulled;
+// layer1 combine CTAs (mode 1, [l[1].n_compute, grid)) never compute.
+struct KernelArgs {
+  LayerArgs l[2];
+  int mode;
+  uint32_t* sched;   // [0] unit claim counter, [1] CTA exit counter (both reset by the last CTA)
+  uint32_t* h_cnt;   // [n_h] mode 2: layer0 half-units completed per 128-row H tile (reset at exit)
+  int n_h;
 };
 
 }  // namespace comet

@@ -52,22 +52,25 @@ constexpr uint32_t kSmemEpiWarp = 32 * 128;              // one warp's 32 rows x
 constexpr uint32_t kSmemEpi = 2 * 4 * kSmemEpiWarp;      // double-buffered, 4 epilogue warps
 
 struct Unit {
-  int pair, nb;
-  int half;  // -1: full 512-column unit; 0/1: one 256-column half (tail split)
+  int layer, pair, nb;
+  int half;  // -1: full 512-column unit; 0/1: one 256-column half
 };
 
-// Tail split (layer0): when the last round of full units would leave at
-// least half the pairs idle, its units are cut into 256-column halves so the
-// tail takes half a unit time instead of a full one.  Units [0, R*n_pairs)
-// stay full; unit R*n_pairs + v is half (v & 1) of full unit R*n_pairs + v/2.
+// A layer's unit sequence: units [0, full) are full 512-column units; unit
+// full + v is half (v & 1) of full unit full + v/2.  Layer0 alone cuts a
+// mostly idle last round into halves (the tail takes half a unit time); layer1
+// splits its last `split_units` units (the end of the launch in modes 1/2).
 struct Sched {
-  int full;   // full units before the tail
-  int total;  // units in the loop (full + halves)
+  int full;   // full units before the split tail
+  int total;  // units in the sequence (full + halves)
 };
-__device__ __forceinline__ Sched make_sched(int U, int n_pairs, bool split) {
-  const int R = U / n_pairs, rem = U - R * n_pairs;
-  if (split && rem > 0 && 2 * rem <= n_pairs) return {R * n_pairs, R * n_pairs + 2 * rem};
-  return {U, U};
+__device__ __forceinline__ Sched make_sched(int U, int n_split) {
+  n_split = max(0, min(U, n_split));
+  return {U - n_split, U + n_split};
+}
+__device__ __forceinline__ int layer0_split(int U, int n_pairs) {
+  const int rem = U % n_pairs;
+  return (rem > 0 && 2 * rem <= n_pairs) ? rem : 0;
 }
 
 // Timeline record: interval [t0, t1] of `role` for unit `task` on this CTA
@@ -88,9 +91,14 @@ __device__ __forceinline__ void tl_record(const LayerArgs& p, int role, int idx,
 //          273-296, at wave granularity: a wave's reduce chunks complete
 //          together); inside a wave, groups of G2 pairs, n-block middle,
 //          pair inner.
-__device__ __forceinline__ Unit decode_unit(int u, int layer, int P, int NB, int G, int G2) {
+//  raster 2 (layer1 inside the fused launch): groups of G2 pairs outer (the
+//          layer0 groups, so a group's layer1 units become ready together),
+//          then waves of G n-blocks, n-block, pair inner.  For a fixed
+//          n-block pairs still ascend, which the fused combine's fold needs.
+__device__ __forceinline__ Unit decode_unit(int u, int layer, int raster, int P, int NB, int G, int G2) {
   Unit r;
-  if (layer == 0) {
+  r.layer = layer;
+  if (raster == 0) {
     const int per_group = G * NB;
     const int g = u / per_group;
     const int base = g * G;
@@ -98,7 +106,7 @@ __device__ __forceinline__ Unit decode_unit(int u, int layer, int P, int NB, int
     const int rem = u - g * per_group;
     r.nb = rem / ge;
     r.pair = base + rem % ge;
-  } else {
+  } else if (raster == 1) {
     const int per_wave = P * G;
     const int w = u / per_wave;
     const int nb0 = w * G;
@@ -109,6 +117,18 @@ __device__ __forceinline__ Unit decode_unit(int u, int layer, int P, int NB, int
     const int base = g * G2;
     const int ge = min(G2, P - base);
     const int rem2 = rem - g * per_group;
+    r.nb = nb0 + rem2 / ge;
+    r.pair = base + rem2 % ge;
+  } else {
+    const int per_group = G2 * NB;
+    const int g = u / per_group;
+    const int base = g * G2;
+    const int ge = min(G2, P - base);
+    const int rem = u - g * per_group;
+    const int per_wave = ge * G;
+    const int w = rem / per_wave;
+    const int nb0 = w * G;
+    const int rem2 = rem - w * per_wave;
     r.nb = nb0 + rem2 / ge;
     r.pair = base + rem2 % ge;
   }
@@ -159,19 +179,55 @@ __device__ __forceinline__ void fold_row(uint32_t (&acc)[32], const __nv_bfloat1
   }
 }
 
-}  // namespace
+constexpr int kSchedSlots = 2;
+// Readers of each claimed unit id: leader CTA producer + MMA + 4 epilogue
+// warps, peer CTA producer + 4 epilogue warps (all arrive on the leader's
+// slot-empty barrier).
+constexpr uint32_t kSchedReaders = 11;
+// The producer asks for its next unit this many k-blocks before the end of
+// the current unit's loads (~4 us of MMA: covers the claim's atomic and
+// broadcast, keeps the claim-ahead short).
+constexpr int kClaimLead = 8;
 
-__global__ void __launch_bounds__(kThreads, 1)
-moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                 const __grid_constant__ CUtensorMap tm_out, const LayerArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  if (static_cast<int>(blockIdx.x) >= p.n_compute) {
-    if (p.debug & 1) return;
-    if (p.layer == 0) comm::dispatch_rows(p, smem);
-    else comm::combine_reduce(p, smem);
-    return;
+__device__ __forceinline__ int seq_total(const KernelArgs& f, int P, int n_pairs, Sched& s0, Sched& s1) {
+  s0 = {0, 0};
+  s1 = {0, 0};
+  if (f.mode != 1) {
+    const int U0 = P * f.l[0].n_blocks;
+    s0 = make_sched(U0, (f.mode == 0 && f.l[0].split_tail) ? layer0_split(U0, n_pairs) : 0);
   }
+  if (f.mode != 0) s1 = make_sched(P * f.l[1].n_blocks, f.l[1].split_units);
+  return s0.total + s1.total;
+}
+
+// Claimed sequence index -> (layer, pair, n-block, half).
+__device__ __forceinline__ Unit unit_at(const KernelArgs& f, int g, int P, const Sched& s0, const Sched& s1) {
+  int layer = 0;
+  Sched s = s0;
+  if (g >= s0.total) {
+    g -= s0.total;
+    layer = 1;
+    s = s1;
+  }
+  const LayerArgs& p = f.l[layer];
+  Unit w;
+  if (g < s.full) {
+    w = decode_unit(g, layer, p.raster, P, p.n_blocks, p.order_group, p.order_group2);
+    w.half = -1;
+  } else {
+    const int v = g - s.full;
+    w = decode_unit(s.full + (v >> 1), layer, p.raster, P, p.n_blocks, p.order_group, p.order_group2);
+    w.half = v & 1;
+  }
+  return w;
+}
+
+// Compute role of a 2-CTA pair: scheduler (leader warp 3) claims units and
+// broadcasts their ids to both CTAs; warp 0 TMA producer, warp 1 MMA issuer
+// (leader), warps 4-7 epilogue.
+__device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem, const CUtensorMap* tm_a0,
+                                             const CUtensorMap* tm_b0, const CUtensorMap* tm_a1,
+                                             const CUtensorMap* tm_b1) {
   uint8_t* epi_smem = smem + kStages * kSmemStage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kSmemEpi);
   uint64_t* full = bars;
@@ -179,19 +235,30 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
   uint64_t* tfull = bars + 2 * kStages;       // accumulators ready (one per unit)
   uint64_t* tempty = bars + 2 * kStages + 1;  // [2]: accumulator half drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 3);
+  uint64_t* sfull = bars + 2 * kStages + 4;                   // [kSchedSlots] unit id written
+  uint64_t* sempty = sfull + kSchedSlots;                     // [kSchedSlots] unit id read by all
+  uint64_t* sreq = sempty + kSchedSlots;                      // producer asks for the next unit
+  int* sunit = reinterpret_cast<int*>(sreq + 1);              // [kSchedSlots]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = blockIdx.x & 1;  // rank in the 2-CTA cluster
-  const bool spin = (p.debug & 4) != 0;
+  const bool leader = cta == 0;
+  const int dbg = f.l[f.mode == 1 ? 1 : 0].debug;
+  const bool spin = (dbg & 4) != 0;
   auto wait = [spin](uint64_t* bar, uint32_t parity) {
     if (spin) ptx::mbar_wait_spin(bar, parity);
     else ptx::mbar_wait(bar, parity);
   };
-  const bool leader = cta == 0;
 
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tm_a);
-    ptx::prefetch_tmap(&tm_b);
+    if (f.mode != 1) {
+      ptx::prefetch_tmap(tm_a0);
+      ptx::prefetch_tmap(tm_b0);
+    }
+    if (f.mode != 0) {
+      ptx::prefetch_tmap(tm_a1);
+      ptx::prefetch_tmap(tm_b1);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -201,6 +268,11 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
     ptx::mbar_init(tfull, 1);
     ptx::mbar_init(tempty + 0, 2 * 128);
     ptx::mbar_init(tempty + 1, 2 * 128);
+    for (int s = 0; s < kSchedSlots; ++s) {
+      ptx::mbar_init(sfull + s, 1);
+      ptx::mbar_init(sempty + s, kSchedReaders);
+    }
+    ptx::mbar_init(sreq, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, kTmemCols);
@@ -209,59 +281,95 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
   ptx::tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
 
-  const int P = p.meta[kMetaPairs];
-  const int NB = p.n_blocks;
-  const int pair_id = blockIdx.x >> 1;
-  const int n_pairs = p.n_compute >> 1;
-  const Sched sch = make_sched(P * NB, n_pairs, p.layer == 0 && p.split_tail);
-  const int U = sch.total;
-  auto unit_of = [&](int u) {
-    Unit w;
-    if (u < sch.full) {
-      w = decode_unit(u, p.layer, P, NB, p.order_group, p.order_group2);
-      w.half = -1;
-    } else {
-      const int v = u - sch.full;
-      w = decode_unit(sch.full + (v >> 1), p.layer, P, NB, p.order_group, p.order_group2);
-      w.half = v & 1;
+  const int P = f.l[f.mode == 1 ? 1 : 0].meta[kMetaPairs];
+  // pairs that compute: everything but layer1 combine CTAs (dispatch CTAs join)
+  const int n_pairs = (f.mode == 1 ? f.l[1].n_compute : static_cast<int>(gridDim.x)) >> 1;
+  Sched s0, s1;
+  const int total = seq_total(f, P, n_pairs, s0, s1);
+  if (f.mode != 0) {
+    const LayerArgs& p1 = f.l[1];
+    if (p1.world > 1 && P == 0 && p1.n_compute == static_cast<int>(gridDim.x) && blockIdx.x == 0 &&
+        threadIdx.x == 0)  // nothing hosted, no combine CTAs: publish empty blocks
+      for (int nb = 0; nb < p1.n_blocks; ++nb)
+        for (int d = 0; d < p1.world; ++d) ptx::st_release_sys(p1.cb_flag_peer[d] + p1.rank * p1.n_blocks + nb, p1.epoch);
+  }
+  // Reader side of the unit ring: lane 0 takes claim i, the warp gets it.
+  auto next_unit = [&](int i) -> int {
+    int g = 0;
+    if (lane == 0) {
+      const int slot = i % kSchedSlots;
+      ptx::mbar_wait_cluster(sfull + slot, (i / kSchedSlots) & 1);
+      g = reinterpret_cast<volatile int*>(sunit)[slot];
+      if (leader) ptx::mbar_arrive(sempty + slot);
+      else ptx::mbar_arrive_cluster(sempty + slot, 0);
     }
-    return w;
+    return __shfl_sync(0xffffffffu, g, 0);
   };
-  if (p.layer == 1 && p.world > 1 && P == 0 && gridDim.x == static_cast<unsigned>(p.n_compute) &&
-      blockIdx.x == 0 && threadIdx.x == 0)  // nothing hosted, no combine CTAs: publish empty blocks
-    for (int nb = 0; nb < NB; ++nb)
-      for (int d = 0; d < p.world; ++d) ptx::st_release_sys(p.cb_flag_peer[d] + p.rank * NB + nb, p.epoch);
 
-  if (warp == 0) {
+  if (warp == 3) {
+    // ---------------- scheduler (leader CTA, one thread) ----------------
+    // Claims just in time: unit i+1 is claimed when the producer asks for it,
+    // a few k-blocks before the end of unit i's loads -- a pair never holds a
+    // queued unit that an idle pair could have run (the tail is units of up
+    // to ~150 us).
+    if (leader && lane == 0) {
+      for (int i = 0;; ++i) {
+        const int slot = i % kSchedSlots;
+        if (i > 0) ptx::mbar_wait(sreq, (i - 1) & 1);
+        ptx::mbar_wait(sempty + slot, ((i / kSchedSlots) & 1) ^ 1);
+        int g = static_cast<int>(atomicAdd(f.sched, 1u));
+        if (g >= total) g = -1;
+        sunit[slot] = g;
+        ptx::st_shared_cluster(sunit + slot, 1, static_cast<uint32_t>(g));
+        ptx::mbar_arrive(sfull + slot);
+        ptx::mbar_arrive_release_cluster(sfull + slot, 1);
+        if (g < 0) break;
+      }
+    }
+  } else if (warp == 0) {
     // ---------------- TMA producer ----------------
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const Unit w = unit_of(u);
+    for (int it = 0;; ++it) {
+      const int g = next_unit(it);
+      if (g < 0) break;
+      const Unit w = unit_at(f, g, P, s0, s1);
+      const LayerArgs& p = f.l[w.layer];
+      const CUtensorMap* ta = w.layer ? tm_a1 : tm_a0;
+      const CUtensorMap* tb = w.layer ? tm_b1 : tm_b0;
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta) + (w.half > 0 ? kHalfN : 0);
-      if (p.layer == 0 && ((pr.w >> cta) & 1) && !(p.debug & 1) && lane == 0) {
-        // this CTA's 128 A rows include rows pulled over NVLink by a comm CTA
-        const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
-        while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) __nanosleep(32);
-        ptx::fence_async_global();
+      if (lane == 0) {
+        if (w.layer == 0 && ((pr.w >> cta) & 1) && !(p.debug & 1)) {
+          // this CTA's 128 A rows include rows pulled over NVLink by a dispatch CTA
+          const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
+          while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) __nanosleep(32);
+          ptx::fence_async_global();
+        } else if (w.layer == 1 && f.mode == 2) {
+          // layer1 A = H rows written by the layer0 epilogues of this launch
+          const uint32_t* hc = f.h_cnt + (row0 >> 7);
+          const uint32_t target = 2u * static_cast<uint32_t>(f.l[0].n_blocks);
+          while (ptx::ld_acquire_gpu(hc) < target) __nanosleep(32);
+          ptx::fence_async_global();
+        }
       }
       __syncwarp();
       const uint64_t t_start = ptx::globaltimer();  // load interval starts once its A rows are ready
+      const int kb_req = max(0, p.k_blocks - kClaimLead);
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         wait(empty + stage, phase ^ 1);
+        if (kb == kb_req && leader && lane == 0) ptx::mbar_arrive(sreq);  // claim the next unit now
         if (lane == 0 && (p.debug & 16)) {
           // debug: no data movement, complete the stage by arrivals only
           if (leader) ptx::mbar_arrive(full + stage);
           else ptx::mbar_arrive_cluster(full + stage, 0);
         } else if (lane == 0) {
           uint8_t* sa = smem + stage * kSmemStage;
-          ptx::tma_load_2d_2sm(sa, &tm_a, full + stage, kb * kBlockK, row0, ptx::kEvictNormal);
-          ptx::tma_load_2d_2sm(sa + kSmemA, &tm_b, full + stage, kb * kBlockK, brow, ptx::kEvictNormal);
+          ptx::tma_load_2d_2sm(sa, ta, full + stage, kb * kBlockK, row0, ptx::kEvictNormal);
+          ptx::tma_load_2d_2sm(sa + kSmemA, tb, full + stage, kb * kBlockK, brow, ptx::kEvictNormal);
           if (w.half < 0)
-            ptx::tma_load_2d_2sm(sa + kSmemA + kSmemBh, &tm_b, full + stage, kb * kBlockK, brow + kHalfN,
+            ptx::tma_load_2d_2sm(sa + kSmemA + kSmemBh, tb, full + stage, kb * kBlockK, brow + kHalfN,
                                  ptx::kEvictNormal);
           if (leader) ptx::mbar_arrive_expect_tx(full + stage, w.half < 0 ? 2 * kSmemStage : 2 * (kSmemA + kSmemBh));
           else ptx::mbar_arrive_cluster(full + stage, 0);
@@ -269,15 +377,18 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) tl_record(p, kRoleLoad, it, u, t_start, ptx::globaltimer());
+      if (lane == 0) tl_record(p, kRoleLoad, it, g, t_start, ptx::globaltimer());
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader CTA, one thread) ----------------
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const bool two = unit_of(u).half < 0;  // both accumulator halves (else only half 0)
+    for (int it = 0;; ++it) {
+      const int g = next_unit(it);
+      if (g < 0) break;
+      const Unit w = unit_at(f, g, P, s0, s1);
+      const LayerArgs& p = f.l[w.layer];
+      const bool two = w.half < 0;  // both accumulator halves (else only half 0)
       const uint32_t ephase = (it & 1) ^ 1;  // previous unit's drain of each half
       const uint64_t t_w = ptx::globaltimer();
       wait(tempty + 0, ephase);
@@ -314,25 +425,29 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
       if (lane == 0) {
-        tl_record(p, kRoleTmemWait, it, u, t_w, t_m);
-        tl_record(p, kRoleMma, it, u, t_m, ptx::globaltimer());
+        tl_record(p, kRoleTmemWait, it, g, t_w, t_m);
+        tl_record(p, kRoleMma, it, g, t_m, ptx::globaltimer());
       }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global ----------------
     const int ew = warp - 4;
-    int it = 0;
-    for (int u = pair_id; u < U; u += n_pairs, ++it) {
-      const Unit w = unit_of(u);
+    for (int it = 0;; ++it) {
+      const int g = next_unit(it);
+      if (g < 0) break;
+      const Unit w = unit_at(f, g, P, s0, s1);
+      const LayerArgs& p = f.l[w.layer];
+      const int NB = p.n_blocks;
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       wait(tfull, it & 1);
       ptx::tc_fence_after();
       const uint64_t t_e = ptx::globaltimer();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
-      const int col0 = w.half > 0 ? static_cast<int>(kHalfN) : 0;           // tail half unit: its columns
-      const int cols_left = p.out_ld - w.nb * kBlockN - col0;  // ragged last n-block (e.g. K/tp = 3200)
+      const int col0 = w.half > 0 ? static_cast<int>(kHalfN) : 0;  // half unit: its columns
+      const int cols_left = p.out_ld - w.nb * kBlockN - col0;      // ragged last n-block (e.g. K/tp = 3200)
       const int n_chunks = w.half < 0 ? static_cast<int>(kBlockN / 64) : static_cast<int>(kHalfN / 64);
+      const int h_lo = w.half < 0 ? 0 : w.half, h_hi = w.half < 0 ? 1 : w.half;  // 256-col halves covered
       // Destination of this lane's row: the layer output, or -- fused combine,
       // the row of its token's last hosted expert -- the token's weighted sum
       // over its hosted experts (executor.py:102-120), written to y (world 1)
@@ -341,22 +456,24 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
       __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN + col0;
       float scale = 1.f;
       int fold_t = -1, fold_s = 0;  // token and own slot of a last-hosted row
-      if (p.layer == 1 && p.fuse_combine) {
+      if (w.layer == 1 && p.fuse_combine) {
         const int rd = p.row_dst[my_row];
         if (rd >= 0) {
           __nv_bfloat16* base = p.world > 1 ? p.cb_peer[rd >> 24] : p.y_local;
-          my_dst = base + static_cast<long long>(rd & 0xFFFFFF) * p.n_embed + w.nb * kBlockN;
+          my_dst = base + static_cast<long long>(rd & 0xFFFFFF) * p.n_embed + w.nb * kBlockN + col0;
           const int widx = p.row_widx[my_row];
           fold_t = widx / p.topk;
           fold_s = widx - fold_t * p.topk;
           if (p.combine_w) scale = p.combine_w[widx];
-          // earlier hosted rows live in pairs claimed before this one (same
-          // n-block, lower unit index): wait for their 128-row tiles
+          // earlier hosted rows live in units claimed before this one (same
+          // n-block columns, lower sequence index): wait for their tiles
           for (int s2 = 0; s2 < fold_s; ++s2) {
             const int pos = p.tok_pos[fold_t * p.topk + s2];
             if (pos < 0) continue;
-            const uint32_t* f = p.tile_done + static_cast<long long>(pos >> 7) * NB + w.nb;
-            while (!ptx::epoch_reached(ptx::ld_acquire_gpu(f), p.epoch)) __nanosleep(64);
+            for (int h = h_lo; h <= h_hi; ++h) {
+              const uint32_t* fl = p.tile_done + (static_cast<long long>(pos >> 7) * NB + w.nb) * 2 + h;
+              while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(64);
+            }
           }
         }
       }
@@ -382,7 +499,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
         ptx::tmem_ld_wait();
         if (half_end) {
           // accumulator half drained: the next unit's MMAs may overwrite it
-          // (a tail half unit used only half 0: release both)
+          // (a half unit used only half 0: release both)
           ptx::tc_fence_before();
           const int h = s * 64 >= static_cast<int>(kHalfN);
           if (leader) ptx::mbar_arrive(tempty + h);
@@ -393,7 +510,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           }
         }
         if (s * 64 >= cols_left || (p.debug & 64)) continue;
-        if (p.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
+        if (w.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             v0[i] = __float_as_uint(__uint_as_float(v0[i]) * scale);
@@ -403,13 +520,14 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
             const int pos = p.tok_pos[fold_t * p.topk + s2];
             if (pos < 0) continue;
             const float ws = p.combine_w ? p.combine_w[fold_t * p.topk + s2] : 1.f;
-            const __nv_bfloat16* src = p.yrows + static_cast<long long>(pos) * p.n_embed + w.nb * kBlockN + s * 64;
+            const __nv_bfloat16* src =
+                p.yrows + static_cast<long long>(pos) * p.n_embed + w.nb * kBlockN + col0 + s * 64;
             fold_row(v0, src, ws);
             fold_row(v1, src + 32, ws);
           }
         }
         uint32_t pk[32];
-        switch (p.activation) {
+        switch (w.layer == 1 ? static_cast<int>(kActIdentity) : p.activation) {
           case kActRelu: pack_chunk<kActRelu>(v0, v1, pk); break;
           case kActSilu: pack_chunk<kActSilu>(v0, v1, pk); break;
           case kActGeluTanh: pack_chunk<kActGeluTanh>(v0, v1, pk); break;
@@ -432,24 +550,37 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
           const int r = i * 4 + rsub;
           const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 128 + ((gsub ^ (r & 7)) * 16));
           __nv_bfloat16* rp = reinterpret_cast<__nv_bfloat16*>(__shfl_sync(0xffffffffu, my_addr, r));
-          if (p.layer == 1) ptx::st_v4(rp + s * 64 + gsub * 8, v);  // re-read by the fold / combine
+          if (w.layer == 1 || f.mode == 2) ptx::st_v4(rp + s * 64 + gsub * 8, v);  // re-read in this launch
           else ptx::st_v4_cs(rp + s * 64 + gsub * 8, v);
         }
         __syncwarp();
       }
-      if (p.layer == 1) {
+      const uint32_t amount = w.half < 0 ? 2u : 1u;  // completion counted in 256-column halves
+      if (w.layer == 0 && f.mode == 2) {
+        // this CTA's 128 H rows of the unit's columns are in memory -> count
+        // them for the layer1 units that read the tile as their A operand
+        ptx::fence_async_global();
+        ptx::named_bar_sync(1, 128);
+        if (threadIdx.x == kEpiThread0) {
+          __threadfence();
+          ptx::red_release_gpu_add(f.h_cnt + (row0 >> 7), amount);
+        }
+      } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
         if (p.world > 1) __threadfence_system();  // pushed rows visible to the peer first
         ptx::named_bar_sync(1, 128);
         if (threadIdx.x == kEpiThread0) {
           __threadfence();
-          ptx::red_release_gpu_add(p.nb_done + w.nb, 1u);
-          if (p.fuse_combine) ptx::st_release_gpu(p.tile_done + static_cast<long long>(row0 >> 7) * NB + w.nb, p.epoch);
+          ptx::red_release_gpu_add(p.nb_done + w.nb, amount);
+          if (p.fuse_combine)
+            for (int h = h_lo; h <= h_hi; ++h)
+              ptx::st_release_gpu(p.tile_done + (static_cast<long long>(row0 >> 7) * NB + w.nb) * 2 + h, p.epoch);
           if (p.world > 1)
-            comm::nb_contributed(p, w.nb, 2u * static_cast<uint32_t>(P) + (gridDim.x - p.n_compute));
+            comm::nb_contributed(p, w.nb, amount,
+                                 4u * static_cast<uint32_t>(P) + (gridDim.x - static_cast<uint32_t>(p.n_compute)));
         }
       }
-      if (threadIdx.x == kEpiThread0) tl_record(p, kRoleEpilogue, it, u, t_e, ptx::globaltimer());
+      if (threadIdx.x == kEpiThread0) tl_record(p, kRoleEpilogue, it, g, t_e, ptx::globaltimer());
     }
   }
 
@@ -458,11 +589,54 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant
   if (warp == 2) ptx::tmem_dealloc_2sm(tmem_base, kTmemCols);
 }
 
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1)
+moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_b0,
+                 const __grid_constant__ CUtensorMap tm_a1, const __grid_constant__ CUtensorMap tm_b1,
+                 const __grid_constant__ KernelArgs f) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_last;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int b = static_cast<int>(blockIdx.x);
+  bool compute = true;
+  if (f.mode == 1 && b >= f.l[1].n_compute) {
+    // layer1 combine CTA (world 1, comm-CTA combine): reduces to the end
+    if (!(f.l[1].debug & 1)) comm::combine_reduce(f.l[1], smem);
+    compute = false;
+  } else if (f.mode != 1 && b >= f.l[0].n_compute) {
+    // layer0 dispatch CTA: pull the remote rows, then join the compute pairs
+    if (!(f.l[0].debug & 1)) comm::dispatch_rows(f.l[0], smem);
+    __syncthreads();
+    comm::comm_release(f.l[0], smem);
+    __syncthreads();
+  }
+  if (compute) compute_role(f, smem, &tm_a0, &tm_b0, &tm_a1, &tm_b1);
+
+  // The last CTA out resets the launch's claim counter and H-tile counters
+  // (nothing reads them after every CTA has left).
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(f.sched + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int i = threadIdx.x; i < f.n_h; i += blockDim.x) f.h_cnt[i] = 0u;
+    if (threadIdx.x == 0) {
+      f.sched[0] = 0u;
+      f.sched[1] = 0u;
+    }
+    __threadfence();
+  }
+}
+
 // Final combine on the source rank (world > 1): sum the partial rows pushed by
 // every contributing rank, ascending rank order (executor.py:239-245 for TP,
-// 102-120 for experts split across EP groups).  One warp per token: the
-// contributor list is built once, then every lane streams 16 B columns of all
-// contributors with several loads in flight.
+// 102-120 for experts split across EP groups).  One warp per (token, 1024-
+// column segment): the contributor list comes from the token's router row,
+// then each lane issues all its 16 B loads of every contributor before
+// summing (latency-bound: ~8 loads in flight per lane, whole GPU).
 __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb,
                                                              const uint32_t* cb_flag, const int32_t* experts) {
   const int NB = p.n_blocks, N = p.n_embed, K = p.topk, W = p.world;
@@ -474,7 +648,12 @@ __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, 
   const int lane = threadIdx.x & 31;
   const int vec = N / 8;
   constexpr int kU = 4;
-  for (int lt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; lt < n_own; lt += (gridDim.x * blockDim.x) >> 5) {
+  constexpr int kSegVec = 32 * kU;  // 16 B vectors per segment
+  const int n_seg = (vec + kSegVec - 1) / kSegVec;
+  const long long items = static_cast<long long>(n_own) * n_seg;
+  for (long long item = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; item < items;
+       item += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const int lt = static_cast<int>(item / n_seg), seg = static_cast<int>(item % n_seg);
     const int t = start + lt;
     // contributing ranks: every TP rank of each distinct EP group of t's
     // experts (ascending experts -> ascending groups -> ascending ranks)
@@ -486,39 +665,38 @@ __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, 
       if (g != last) groups[ng++] = g;
       last = g;
     }
-    for (int c0 = lane; c0 < vec; c0 += 32 * kU) {
-      float acc[kU][8];
+    const int c0 = seg * kSegVec + lane;
+    float acc[kU][8];
 #pragma unroll
-      for (int u = 0; u < kU; ++u)
+    for (int u = 0; u < kU; ++u)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[u][j] = 0.f;
-      for (int gi = 0; gi < ng; ++gi) {
-        for (int r = groups[gi] * p.tp; r < (groups[gi] + 1) * p.tp; ++r) {
-          const __nv_bfloat16* row = cb + (static_cast<long long>(r) * p.mloc_cap + lt) * N;
-          uint4 v[kU];
+      for (int j = 0; j < 8; ++j) acc[u][j] = 0.f;
+    for (int gi = 0; gi < ng; ++gi) {
+      for (int r = groups[gi] * p.tp; r < (groups[gi] + 1) * p.tp; ++r) {
+        const __nv_bfloat16* row = cb + (static_cast<long long>(r) * p.mloc_cap + lt) * N;
+        uint4 v[kU];
 #pragma unroll
-          for (int u = 0; u < kU; ++u)
-            v[u] = c0 + u * 32 < vec ? ptx::ld_v4(row + (c0 + u * 32) * 8) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < kU; ++u)
+          v[u] = c0 + u * 32 < vec ? ptx::ld_v4(row + (c0 + u * 32) * 8) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+        for (int u = 0; u < kU; ++u) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 f = __bfloat1622float2(h[j]);
-              acc[u][2 * j] += f.x;
-              acc[u][2 * j + 1] += f.y;
-            }
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(h[j]);
+            acc[u][2 * j] += f.x;
+            acc[u][2 * j + 1] += f.y;
           }
         }
       }
+    }
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (c0 + u * 32 >= vec) continue;
-        uint4 o;
-        o.x = pack_bf16(acc[u][0], acc[u][1]); o.y = pack_bf16(acc[u][2], acc[u][3]);
-        o.z = pack_bf16(acc[u][4], acc[u][5]); o.w = pack_bf16(acc[u][6], acc[u][7]);
-        ptx::st_v4(p.y_local + static_cast<long long>(lt) * N + (c0 + u * 32) * 8, o);
-      }
+    for (int u = 0; u < kU; ++u) {
+      if (c0 + u * 32 >= vec) continue;
+      uint4 o;
+      o.x = pack_bf16(acc[u][0], acc[u][1]); o.y = pack_bf16(acc[u][2], acc[u][3]);
+      o.z = pack_bf16(acc[u][4], acc[u][5]); o.w = pack_bf16(acc[u][6], acc[u][7]);
+      ptx::st_v4(p.y_local + static_cast<long long>(lt) * N + (c0 + u * 32) * 8, o);
     }
   }
 }

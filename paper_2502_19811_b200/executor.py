@@ -325,6 +325,14 @@ def index_flags(world: int, n_comm1: int) -> int:
     return (2 if world == 1 and n_comm1 > 0 else 0) | (4 if world > 1 else 0)
 
 
+def fused_launch(world: int, n_comm1: int) -> bool:
+    """Both layers in one persistent launch (comet_layers) -- the default,
+    as in comet_forward -- unless world-1 combine CTAs are asked for or
+    COMET_FUSED=0."""
+    import os
+    return os.environ.get("COMET_FUSED", "1") != "0" and not (world == 1 and n_comm1 > 0)
+
+
 def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
     """Enqueue a forward of every emulated rank, phase by phase, on one
     stream: each in-kernel wait is on work enqueued before it, so ranks that
@@ -335,13 +343,19 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
         # hot path: the kernels' tables only (+ the combine list for world-1
         # combine CTAs); world > 1: the build also publishes the x_ready epoch
         layer.ctx.index_build(ex, M, stream=stream, flags=index_flags(world, layer.n_comm1()))
-    for layer in layers:
-        k = layer.knobs
-        layer.ctx.layer0(layer.weights.w0t, layer.act, k.n_comm0 if world > 1 else 0, k.group0, stream=stream)
-    for layer, y in zip(layers, outs):
-        k = layer.knobs
-        layer.ctx.layer1(layer.weights.w1t, cw, y, layer.n_comm1(), k.wave1,
-                         stream=stream)
+    if fused_launch(world, layers[0].n_comm1()):
+        for layer, y in zip(layers, outs):
+            k = layer.knobs
+            layer.ctx.layers(layer.weights.w0t, layer.weights.w1t, cw, y, layer.act,
+                             k.n_comm0 if world > 1 else 0, k.group0, k.wave1, stream=stream)
+    else:
+        for layer in layers:
+            k = layer.knobs
+            layer.ctx.layer0(layer.weights.w0t, layer.act, k.n_comm0 if world > 1 else 0, k.group0, stream=stream)
+        for layer, y in zip(layers, outs):
+            k = layer.knobs
+            layer.ctx.layer1(layer.weights.w1t, cw, y, layer.n_comm1(), k.wave1,
+                             stream=stream)
     if world > 1:
         for layer, y in zip(layers, outs):
             layer.ctx.combine_finish(y, stream=stream)

@@ -139,11 +139,12 @@ class EmulatedGroup:
     def _forward_timed(self, record: bool):
         """One forward, phase-ordered over the emulated ranks (ranks share a
         device, so each in-kernel wait is on work enqueued before it)."""
-        from .executor import index_flags
+        from .executor import fused_launch, index_flags
         torch = self.torch
         W = self.parallel.world_size
         ev = (lambda: torch.cuda.Event(enable_timing=True)) if record else (lambda: None)
-        rec = {k: [] for k in ("index", "layer0", "layer1", "finish")}
+        fused = fused_launch(W, self.layers[0].n_comm1())
+        rec = {k: [] for k in (("index", "layers", "finish") if fused else ("index", "layer0", "layer1", "finish"))}
 
         def timed(key, fn):
             a, b = ev(), ev()
@@ -156,11 +157,18 @@ class EmulatedGroup:
 
         for l in self.layers:
             timed("index", lambda l=l: l.ctx.index_build(self.ex, self.M, flags=index_flags(W, l.n_comm1())))
-        for l in self.layers:
-            k = l.knobs
-            timed("layer0", lambda l=l, k=k: l.ctx.layer0(l.weights.w0t, l.act, k.n_comm0 if W > 1 else 0, k.group0))
-        for l, y in zip(self.layers, self.ys):
-            timed("layer1", lambda l=l, y=y: l.ctx.layer1(l.weights.w1t, None, y, l.n_comm1(), l.knobs.wave1))
+        if fused:
+            for l, y in zip(self.layers, self.ys):
+                k = l.knobs
+                timed("layers", lambda l=l, y=y, k=k: l.ctx.layers(l.weights.w0t, l.weights.w1t, None, y, l.act,
+                                                                   k.n_comm0 if W > 1 else 0, k.group0, k.wave1))
+        else:
+            for l in self.layers:
+                k = l.knobs
+                timed("layer0", lambda l=l, k=k: l.ctx.layer0(l.weights.w0t, l.act, k.n_comm0 if W > 1 else 0,
+                                                              k.group0))
+            for l, y in zip(self.layers, self.ys):
+                timed("layer1", lambda l=l, y=y: l.ctx.layer1(l.weights.w1t, None, y, l.n_comm1(), l.knobs.wave1))
         for l, y in zip(self.layers, self.ys):
             timed("finish", lambda l=l, y=y: l.ctx.combine_finish(y))
         return rec

@@ -114,7 +114,10 @@ def audit(intervals: Sequence[Interval], deps: Dict[int, List[int]] = None) -> L
             if c.start_ns < a.end_ns and a.block_kind == c.block_kind:
                 problems.append(f"block {b}: [{a.start_ns},{a.end_ns}) overlaps [{c.start_ns},{c.end_ns})")
     if deps:
-        comm_end = {iv.task_id: iv.end_ns for iv in intervals if iv.block_kind == "comm"}
+        comm_end: Dict[int, int] = {}  # a task split over several intervals ends with its last
+        for iv in intervals:
+            if iv.block_kind == "comm":
+                comm_end[iv.task_id] = max(comm_end.get(iv.task_id, iv.end_ns), iv.end_ns)
         for iv in intervals:
             if iv.block_kind != "compute":
                 continue

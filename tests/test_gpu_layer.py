@@ -165,3 +165,31 @@ def test_mixtral_full_size_vs_torch_fp32_and_determinism():
     ref = torch_reference(x, w0, w1, ex.long(), combine_w=cw)
     assert_close(y1.float().cpu().numpy(), ref.cpu().numpy(), what="Mixtral M=8192 EP=1")
     layer.close()
+
+
+@pytest.mark.parametrize("tp,ep,topk,std", [(1, 1, 2, 0.032), (1, 4, 2, 0.05), (1, 8, 2, 0.0), (2, 2, 3, 0.032),
+                                            (1, 2, 8, 0.0)])
+def test_launch_modes_bitwise_equal(tp, ep, topk, std, monkeypatch):
+    """One fused launch for both layers (dynamic unit claims, layer1 tiles
+    gated on per-tile H counters, dispatch CTAs joining the GEMMs) vs
+    separate layer0 / layer1 launches, and every layer1 tail split: each
+    output element accumulates the same products in the same order, so the
+    results are bitwise identical -- and match the oracle."""
+    E = 16 if topk == 8 else 8
+    model = ModelConfig(L=1, E=E, topk=topk, N=512, K=1024)
+    par = ParallelSpec(tp, ep)
+    routing = build_routing(model, par, WorkloadSpec(M=1500, seed=21, std=std))
+    w = random_weights(model, seed=22)
+    x = np.random.default_rng(23).standard_normal((1500, 512))
+    cw = np.random.default_rng(24).random((1500, topk))
+    outs = []
+    for fused, split1 in (("0", "0"), ("1", "0"), ("1", "74"), ("1", "100000")):
+        monkeypatch.setenv("COMET_FUSED", fused)
+        monkeypatch.setenv("COMET_SPLIT1", split1)
+        outs.append(run_emulated(x, w, routing, par, activation="silu", combine_weights=cw,
+                                 knobs=LayerKnobs(n_comm0=4, n_comm1=0)).cpu().numpy())
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+    silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), silu, cw, tp=tp)
+    assert_close(outs[0], ref, what=f"modes tp={tp} ep={ep} topk={topk}")

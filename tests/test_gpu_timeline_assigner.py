@@ -63,10 +63,13 @@ def test_measured_timeline_overlap_and_dependency_audit():
         # NVLink tile holding its 128 A rows (tile 2*pair + cta) was published
         meta = layer.ctx.index_meta()
         P, NB = int(meta[3]), -(-layer.ctx.k_local // 512)
+        # (a tile's remote rows are pulled in 16-row chunks by several dispatch
+        # CTAs: one comm interval per chunk, task = tile; the audit takes the
+        # tile's last chunk)
         comm_ivs = [TL.Interval(c, "comm", t, s, e) for c, r, t, s, e in recs if r == "comm"]
-        assert len({iv.task_id for iv in comm_ivs}) == len(comm_ivs)
         load_ivs = [TL.Interval(c, "compute", 2 * t + (c & 1), s, e) for c, r, t, s, e in recs if r == "load"]
-        n_pairs = (torch.cuda.get_device_properties(0).multi_processor_count // 2 * 2 - knobs.n_comm0) // 2
+        # unit claims are dynamic over every pair (dispatch pairs join the GEMMs)
+        n_pairs = torch.cuda.get_device_properties(0).multi_processor_count // 2
         deps = {2 * u + c: [2 * _decode_layer0(u, P, NB, knobs.group0, n_pairs) + c]
                 for u in range(2 * P * NB) for c in (0, 1)}
         bad = [p for p in TL.audit(comm_ivs + load_ivs, deps) if "overlaps" not in p]
