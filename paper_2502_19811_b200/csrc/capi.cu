@@ -674,7 +674,7 @@ static int layer0_args(comet_ctx* x, const void* w0t, int activation, int n_comm
   a.raster = 0;
   a.activation = activation;
   a.split_tail = env_int("COMET_SPLIT", 1) != 0;
-  a.chunk_rows = std::max(1, std::min(32, env_int("COMET_CHUNK", 16)));
+  a.chunk_rows = std::max(1, std::min(32, env_int("COMET_CHUNK", 32)));
   a.pairs = x->ix.pairs0;
   a.out = x->H;
   a.out_ld = x->k_local;
@@ -781,7 +781,10 @@ int comet_layers(comet_ctx* x, const void* w0t, const void* w1t, const float* co
   // keeps the expert-ascending table (a token's earlier hosted rows must sit
   // in earlier units of the same columns).
   f.l[1].raster = 2;
-  f.l[1].order_group2 = f.l[0].order_group;
+  f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
+  // layer0's last partial round in halves too: the layer1 units of its pairs
+  // wait for it (critical path = last layer0 unit + one layer1 unit)
+  f.l[0].split_tail = env_int("COMET_SPLIT0", 1) != 0;
   if (!f.l[1].fuse_combine || x->E_r == 1 || x->cfg.topk == 1) f.l[1].pairs = x->ix.pairs0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (int rc = dispatch_local(x, st)) return rc;

@@ -194,7 +194,7 @@ __device__ __forceinline__ int seq_total(const KernelArgs& f, int P, int n_pairs
   s1 = {0, 0};
   if (f.mode != 1) {
     const int U0 = P * f.l[0].n_blocks;
-    s0 = make_sched(U0, (f.mode == 0 && f.l[0].split_tail) ? layer0_split(U0, n_pairs) : 0);
+    s0 = make_sched(U0, f.l[0].split_tail ? layer0_split(U0, n_pairs) : 0);
   }
   if (f.mode != 0) s1 = make_sched(P * f.l[1].n_blocks, f.l[1].split_units);
   return s0.total + s1.total;

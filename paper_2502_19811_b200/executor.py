@@ -148,7 +148,7 @@ class LayerKnobs:
     measured timings; group0 / wave1 set the layer0 L2 grouping and the
     layer1 column-wave width."""
 
-    n_comm0: int = 2
+    n_comm0: int = 64
     n_comm1: int = 0
     group0: int = 4
     wave1: int = 4
@@ -237,6 +237,77 @@ class MoELayer:
         y = torch.empty(hi - lo, self.n_pad, dtype=torch.bfloat16, device=dev)
         self.run(ex.contiguous(), M, y, cw)
         return y if self.n_pad == self.model.N else y[:, :self.model.N]
+
+    def forward_host(self, x_host, experts_host, combine_w=None, out=None, chunks: Optional[int] = None):
+        """End-to-end form on HOST buffers (pinned for overlap): H2D of the
+        tokens and router output, the forward, D2H of the result into ``out``
+        (allocated pinned when None); asynchronous on the current stream like
+        ``forward`` (synchronise it before reading ``out``).
+
+        Single GPU: the layer is token-independent, so the M tokens run as
+        ``chunks`` consecutive forwards (default 4 for M >= 8192) with the H2D
+        of chunk c+1 and the D2H of chunk c-1 on two copy streams under the
+        forward of chunk c -- only the first chunk's upload and the last
+        chunk's download stay exposed.  Multi-GPU ranks copy, run, copy."""
+        torch = self.torch
+        M = int(experts_host.shape[0])
+        N = self.model.N
+        lo_r, hi_r = self.token_range(M)
+        if out is None:
+            out = torch.empty(hi_r - lo_r, N, dtype=torch.bfloat16, pin_memory=True)
+        world = self.parallel.world_size
+        C = chunks if chunks is not None else max(1, min(4, M // 2048))
+        if world > 1 or C <= 1:
+            y = self.forward(x_host, experts_host, combine_w, M=M)
+            out.copy_(y, non_blocking=True)
+            return out
+        dev = torch.device("cuda", self.device)
+        bounds = [M * c // C for c in range(C + 1)]
+        mc = max(bounds[i + 1] - bounds[i] for i in range(C))
+        st = getattr(self, "_pipe", None)
+        if st is None or st["mc"] < mc:
+            bf, i32, f32 = torch.bfloat16, torch.int32, torch.float32
+            st = {"mc": mc, "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                  "x": [torch.empty(mc, N, dtype=bf, device=dev) for _ in range(2)],
+                  "ex": [torch.empty(mc, self.model.topk, dtype=i32, device=dev) for _ in range(2)],
+                  "cw": [torch.empty(mc, self.model.topk, dtype=f32, device=dev) for _ in range(2)],
+                  "y": [torch.empty(mc, self.n_pad, dtype=bf, device=dev) for _ in range(2)],
+                  "done": [None, None], "down": [None, None]}
+            self._pipe = st
+        comp = torch.cuda.current_stream(dev)
+        h2d, d2h = st["h2d"], st["d2h"]
+        start = torch.cuda.Event()  # uploads begin after the caller's prior work (honest step timing)
+        start.record(comp)
+        h2d.wait_event(start)
+        last = None
+        for c in range(C):
+            lo, hi = bounds[c], bounds[c + 1]
+            m, b = hi - lo, c % 2
+            with torch.cuda.stream(h2d):
+                if st["done"][b] is not None:  # staging slot b consumed by its last forward
+                    h2d.wait_event(st["done"][b])
+                st["x"][b][:m].copy_(x_host[lo:hi], non_blocking=True)
+                st["ex"][b][:m].copy_(experts_host[lo:hi], non_blocking=True)
+                if combine_w is not None:
+                    st["cw"][b][:m].copy_(combine_w[lo:hi], non_blocking=True)
+                up = torch.cuda.Event()
+                up.record(h2d)
+            comp.wait_event(up)
+            if st["down"][b] is not None:  # output slot b downloaded
+                comp.wait_event(st["down"][b])
+            self._xbuf[:m, :N].copy_(st["x"][b][:m], non_blocking=True)
+            self.run(st["ex"][b][:m], m, st["y"][b][:m], st["cw"][b][:m] if combine_w is not None else None)
+            done = torch.cuda.Event()
+            done.record(comp)
+            st["done"][b] = done
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                out[lo:hi].copy_(st["y"][b][:m, :N], non_blocking=True)
+                last = torch.cuda.Event()
+                last.record(d2h)
+            st["down"][b] = last
+        comp.wait_event(last)
+        return out
 
     def close(self) -> None:
         self.ctx.close()

@@ -193,3 +193,26 @@ def test_launch_modes_bitwise_equal(tp, ep, topk, std, monkeypatch):
     silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
     ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), silu, cw, tp=tp)
     assert_close(outs[0], ref, what=f"modes tp={tp} ep={ep} topk={topk}")
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 4])
+def test_forward_host_pipeline(chunks):
+    """Host-buffer end-to-end form: chunked H2D / forward / D2H pipeline
+    (single GPU) == the device forward on the same tokens."""
+    import torch
+    model = ModelConfig(L=1, E=8, topk=2, N=512, K=1024)
+    par = ParallelSpec()
+    M = 5000
+    routing = build_routing(model, par, WorkloadSpec(M=M, seed=31, std=0.032))
+    w = random_weights(model, seed=32)
+    layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0))
+    x = torch.from_numpy(np.random.default_rng(33).standard_normal((M, 512)).astype(np.float32)).to(torch.bfloat16)
+    ex = torch.from_numpy(routing.as_array().copy())
+    cw = torch.from_numpy(np.random.default_rng(34).random((M, 2)).astype(np.float32))
+    out = layer.forward_host(x.pin_memory(), ex.pin_memory(), cw.pin_memory(), chunks=chunks)
+    out2 = layer.forward_host(x.pin_memory(), ex.pin_memory(), cw.pin_memory(), chunks=chunks)  # slot reuse
+    torch.cuda.synchronize()
+    ref = oracle_bf16_inputs(x.float().numpy(), w.w0, w.w1, routing.as_array(), combine_weights=cw.numpy())
+    assert_close(out.float().numpy(), ref, what=f"forward_host chunks={chunks}")
+    assert torch.equal(out, out2)
+    layer.close()

@@ -66,7 +66,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "matrix.jsonl"))
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--nc0", default="2,4,8", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
+    ap.add_argument("--nc0", default="16,32,64", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
     a = ap.parse_args()
     burst, sust, _, src = load_peaks()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
