@@ -31,7 +31,8 @@ struct LayerArgs {
   int split_tail;         // layer0 (alone): cut a mostly idle last round into 256-column half units
   int split_units;        // layer1: the last `split_units` full units run as 256-column halves
   uint32_t epoch;
-  int debug;              // bit0: comm CTAs idle; bit1: layer0 A by 2D tile (no gather); bit2: spin waits
+  int debug;              // bit0: comm CTAs idle; bit2: spin waits; bit3: no MMA; bit4: no loads;
+                          // bit5: sequential (GEMMs start after the whole dispatch); bit6/7: no stores / no drain
 
   // index (device)
   const int32_t* meta;

@@ -330,6 +330,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
     // ---------------- TMA producer ----------------
     int stage = 0;
     uint32_t phase = 0;
+    bool seq_done = false;
     for (int it = 0;; ++it) {
       const int g = next_unit(it);
       if (g < 0) break;
@@ -340,6 +341,14 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta) + (w.half > 0 ? kHalfN : 0);
+      if (lane == 0 && w.layer == 0 && (p.debug & 32) && !seq_done && !(p.debug & 1)) {
+        // "sequential" mode (no overlap, the cli's baseline): the first GEMM
+        // waits for the WHOLE dispatch, like an all-to-all before GroupGEMM
+        for (int q = 0; q < 2 * P; ++q)
+          if ((reinterpret_cast<const int4*>(p.pairs)[q >> 1].w >> (q & 1)) & 1)
+            while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.xg_ready + q), p.epoch)) __nanosleep(64);
+        seq_done = true;
+      }
       if (lane == 0) {
         if (w.layer == 0 && ((pr.w >> cta) & 1) && !(p.debug & 1)) {
           // this CTA's 128 A rows include rows pulled over NVLink by a dispatch CTA

@@ -245,7 +245,7 @@ class MoELayer:
         ``forward`` (synchronise it before reading ``out``).
 
         Single GPU: the layer is token-independent, so the M tokens run as
-        ``chunks`` consecutive forwards (default 4 for M >= 8192) with the H2D
+        ``chunks`` consecutive forwards (default 3 for M >= 6144) with the H2D
         of chunk c+1 and the D2H of chunk c-1 on two copy streams under the
         forward of chunk c -- only the first chunk's upload and the last
         chunk's download stay exposed.  Multi-GPU ranks copy, run, copy."""
@@ -256,7 +256,7 @@ class MoELayer:
         if out is None:
             out = torch.empty(hi_r - lo_r, N, dtype=torch.bfloat16, pin_memory=True)
         world = self.parallel.world_size
-        C = chunks if chunks is not None else max(1, min(4, M // 2048))
+        C = chunks if chunks is not None else max(1, min(3, M // 2048))  # measured best at M=8192: 3
         if world > 1 or C <= 1:
             y = self.forward(x_host, experts_host, combine_w, M=M)
             out.copy_(y, non_blocking=True)
