@@ -245,10 +245,13 @@ class MoELayer:
         ``forward`` (synchronise it before reading ``out``).
 
         Single GPU: the layer is token-independent, so the M tokens run as
-        ``chunks`` consecutive forwards (default 3 for M >= 6144) with the H2D
-        of chunk c+1 and the D2H of chunk c-1 on two copy streams under the
-        forward of chunk c -- only the first chunk's upload and the last
-        chunk's download stay exposed.  Multi-GPU ranks copy, run, copy."""
+        consecutive forwards over token chunks with the H2D of chunk c+1 and
+        the D2H of chunk c-1 on two copy streams under the forward of chunk
+        c.  Only the first chunk's upload and the last chunk's download stay
+        exposed, so the ends are small and the middle large (default
+        M/8, 3M/8, 3M/8, M/8 for M >= 8192: each middle forward outlasts its
+        neighbours' copies; ``chunks`` = an int for equal chunks or a list of
+        sizes).  Multi-GPU ranks copy, run, copy."""
         torch = self.torch
         M = int(experts_host.shape[0])
         N = self.model.N
@@ -256,14 +259,17 @@ class MoELayer:
         if out is None:
             out = torch.empty(hi_r - lo_r, N, dtype=torch.bfloat16, pin_memory=True)
         world = self.parallel.world_size
-        C = chunks if chunks is not None else max(1, min(3, M // 2048))  # measured best at M=8192: 3
-        if world > 1 or C <= 1:
+        sizes = _chunk_sizes(M, chunks)
+        if world > 1 or len(sizes) <= 1:
             y = self.forward(x_host, experts_host, combine_w, M=M)
             out.copy_(y, non_blocking=True)
             return out
         dev = torch.device("cuda", self.device)
-        bounds = [M * c // C for c in range(C + 1)]
-        mc = max(bounds[i + 1] - bounds[i] for i in range(C))
+        C = len(sizes)
+        bounds = [0]
+        for n in sizes:
+            bounds.append(bounds[-1] + n)
+        mc = max(sizes)
         st = getattr(self, "_pipe", None)
         if st is None or st["mc"] < mc:
             bf, i32, f32 = torch.bfloat16, torch.int32, torch.float32
@@ -311,6 +317,25 @@ class MoELayer:
 
     def close(self) -> None:
         self.ctx.close()
+
+
+def _chunk_sizes(M: int, chunks=None) -> List[int]:
+    """Token chunks of the host pipeline (see MoELayer.forward_host)."""
+    if isinstance(chunks, (list, tuple)):
+        if sum(chunks) != M or any(c <= 0 for c in chunks):
+            raise ConfigurationError(f"chunk sizes {chunks} must be positive and sum to M={M}")
+        return list(chunks)
+    if chunks is not None:
+        C = max(1, min(int(chunks), M))
+        return [M * (c + 1) // C - M * c // C for c in range(C)]
+    if M >= 8192:
+        e = (M // 8) // 256 * 256
+        mid = M - 2 * e
+        return [e, mid // 2, mid - mid // 2, e]
+    if M >= 4096:
+        e = (M // 4) // 256 * 256
+        return [e, M - 2 * e, e]
+    return [M]
 
 
 # ---------------------------------------------------------------------------

@@ -195,7 +195,7 @@ def test_launch_modes_bitwise_equal(tp, ep, topk, std, monkeypatch):
     assert_close(outs[0], ref, what=f"modes tp={tp} ep={ep} topk={topk}")
 
 
-@pytest.mark.parametrize("chunks", [1, 3, 4])
+@pytest.mark.parametrize("chunks", [1, 3, None, [512, 2000, 2000, 488]])
 def test_forward_host_pipeline(chunks):
     """Host-buffer end-to-end form: chunked H2D / forward / D2H pipeline
     (single GPU) == the device forward on the same tokens."""
