@@ -423,7 +423,8 @@ def main():
     ap.add_argument("--std", type=float, default=0.0)
     ap.add_argument("--n-comm0", type=int, default=64)
     ap.add_argument("--n-comm1", type=int, default=0)
-    ap.add_argument("--group0", type=int, default=4)
+    ap.add_argument("--group0", type=int, default=None,
+                    help="layer0 pair-group raster (default: 8 on one GPU, 4 for EP > 1; measured)")
     ap.add_argument("--wave1", type=int, default=4)
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -431,6 +432,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.group0 is None:
+        args.group0 = 8 if args.gpus == 1 else 4
     return run_reference(args) if args.impl == "reference" else run_ours(args)
 
 

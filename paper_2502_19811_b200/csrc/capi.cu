@@ -62,6 +62,11 @@ constexpr size_t kIndexSmem = 8192 * sizeof(long long);
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -147,6 +152,8 @@ struct comet_ctx {
   MapCache w0c, w1c;
   uint32_t* sched = nullptr;  // [2] unit claim / CTA exit counters of the layer kernel (self-resetting)
   uint32_t* h_cnt = nullptr;  // [cap_rows_pad / 128 + 1] fused-launch H tile counters (self-resetting)
+  float* part = nullptr;       // split-K partials: 2 layers x (pairs x 2 CTA tiles) x 128 x 512 fp32
+  uint32_t* split_cnt = nullptr;  // 2 layers x 512 slice counters (reset by each tile's finisher)
   int n_h = 0;
 };
 
@@ -334,6 +341,8 @@ int comet_ctx_destroy(comet_ctx* x) {
   cudaFree(x->tile_done);
   cudaFree(x->sched);
   cudaFree(x->h_cnt);
+  cudaFree(x->part);
+  cudaFree(x->split_cnt);
   cudaFree(x->timeline);
   cudaFree(x->counters);
   cudaFree(x->routing);
@@ -560,6 +569,11 @@ static int ensure_work(comet_ctx* x) {
   CK(cudaMemset(x->sched, 0, sizeof(uint32_t) * 2));
   CK(cudaMalloc(&x->h_cnt, sizeof(uint32_t) * x->n_h));
   CK(cudaMemset(x->h_cnt, 0, sizeof(uint32_t) * x->n_h));
+  // split-K only runs when a layer's output tiles x slices <= pairs: each
+  // layer needs at most (grid/2 pairs) x 2 CTA tiles of 128 x 512 fp32
+  CK(cudaMalloc(&x->part, (size_t)2 * x->n_sm * kTileRows * kBlockN * sizeof(float)));
+  CK(cudaMalloc(&x->split_cnt, sizeof(uint32_t) * 2 * 512));
+  CK(cudaMemset(x->split_cnt, 0, sizeof(uint32_t) * 2 * 512));
   int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
   if (!rc) rc = make_map(&x->tm_xg, x->xg, x->cap_rows_pad, c.N, 128);
   if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
@@ -615,6 +629,7 @@ static LayerArgs base_args(comet_ctx* x) {
   a.nb_done = x->counters;
   a.nb_sent = x->counters + x->nb1;
   a.mloc_cap = x->mloc_cap;
+  a.ksplit_max = std::max(0, std::min(8, env_int("COMET_KSPLIT", 8)));
   a.timeline = x->timeline;
   a.timeline_cap = x->timeline_cap;
   return a;
@@ -626,10 +641,6 @@ static int layer_grid(comet_ctx* x) {
   return grid & ~1;
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 static int launch_kernel(comet_ctx* x, KernelArgs& f, const CUtensorMap& a0, const CUtensorMap& b0,
                          const CUtensorMap& a1, const CUtensorMap& b1, cudaStream_t st) {
@@ -666,6 +677,8 @@ static int layer0_args(comet_ctx* x, const void* w0t, int activation, int n_comm
   if (int rc = get_weight_map(x, x->w0c, w0t, (uint64_t)x->E_r * x->k_local, c.N)) return rc;
   LayerArgs a = base_args(x);
   a.layer = 0;
+  a.part = x->part;
+  a.split_cnt = x->split_cnt;
   a.n_compute = grid - n_comm;
   a.n_blocks = x->nb0;
   a.k_blocks = x->kb0;
@@ -692,6 +705,8 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   if (int rc = get_weight_map(x, x->w1c, w1t, (uint64_t)x->E_r * c.N, x->k_local)) return rc;
   LayerArgs a = base_args(x);
   a.layer = 1;
+  a.part = x->part + (size_t)x->n_sm * kTileRows * kBlockN;
+  a.split_cnt = x->split_cnt + 512;
   a.n_blocks = x->nb1;
   a.k_blocks = x->kb1;
   a.b_rows = c.N;

@@ -249,8 +249,10 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
     }
     int k = 0;
     for (int nb = 0; nb < NB; ++nb) {
+      const int nb_cols = p.out_ld - nb * static_cast<int>(kBlockN);  // a ragged last block <= 256 wide
+      const uint32_t nb_target = (nb_cols > 0 && nb_cols <= static_cast<int>(kBlockN / 2)) ? target / 2 : target;
       if (lane == 0)
-        while (ptx::ld_acquire_gpu(p.nb_done + nb) < target) __nanosleep(128);
+        while (ptx::ld_acquire_gpu(p.nb_done + nb) < nb_target) __nanosleep(128);
       __syncwarp();
       const unsigned long long t_nb = ptx::globaltimer();
       const uint32_t seg = min(kSeg, static_cast<uint32_t>(N - nb * kBlockN) * 2u);
@@ -333,7 +335,11 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
       // all reducers of this CTA finished nb -> count the CTA; last CTA signals peers
       __threadfence_system();
       ptx::named_bar_sync(2, kReducers * 32);
-      if (threadIdx.x == 32) nb_contributed(p, nb, 1u, target + static_cast<uint32_t>(n_comm));
+      if (threadIdx.x == 32) {
+        const int nb_cols = p.out_ld - nb * static_cast<int>(kBlockN);
+        const uint32_t nb_target = (nb_cols > 0 && nb_cols <= static_cast<int>(kBlockN / 2)) ? target / 2 : target;
+        nb_contributed(p, nb, 1u, nb_target + static_cast<uint32_t>(n_comm));
+      }
     }
   }
 }

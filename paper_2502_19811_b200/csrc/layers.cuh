@@ -30,6 +30,9 @@ struct LayerArgs {
   int activation;
   int split_tail;         // layer0 (alone): cut a mostly idle last round into 256-column half units
   int split_units;        // layer1: the last `split_units` full units run as 256-column halves
+  int ksplit_max;         // split-K slices allowed when output tiles are fewer than pairs (0 = off)
+  float* part;            // split-K fp32 partials [tiles*NB][S][128][512] (<= pairs*2 CTA tiles)
+  uint32_t* split_cnt;    // [tiles*NB] slices landed (reset by the finisher)
   uint32_t epoch;
   int debug;              // bit0: comm CTAs idle; bit2: spin waits; bit3: no MMA; bit4: no loads;
                           // bit5: sequential (GEMMs start after the whole dispatch); bit6/7: no stores / no drain

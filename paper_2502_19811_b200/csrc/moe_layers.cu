@@ -54,6 +54,7 @@ constexpr uint32_t kSmemEpi = 2 * 4 * kSmemEpiWarp;      // double-buffered, 4 e
 struct Unit {
   int layer, pair, nb;
   int half;  // -1: full 512-column unit; 0/1: one 256-column half
+  int ks;    // K slice (split-K): k-blocks [ks*KB/S, (ks+1)*KB/S) of S slices
 };
 
 // A layer's unit sequence: units [0, full) are full 512-column units; unit
@@ -63,10 +64,19 @@ struct Unit {
 struct Sched {
   int full;   // full units before the split tail
   int total;  // units in the sequence (full + halves)
+  int S;      // K slices per output tile (split-K; 1 = off)
 };
-__device__ __forceinline__ Sched make_sched(int U, int n_split) {
-  n_split = max(0, min(U, n_split));
-  return {U - n_split, U + n_split};
+__device__ __forceinline__ Sched make_sched(int U, int n_split, int S = 1) {
+  n_split = S > 1 ? 0 : max(0, min(U, n_split));
+  return {U * S - n_split, U * S + n_split, S};
+}
+// Split-K when a layer has too few output tiles to fill the pairs (small M
+// per rank, e.g. Mixtral EP=8 at 1K tokens: 8 layer1 tiles of K = 14336 on
+// 74 pairs): S slices of >= 4 k-blocks, S * tiles <= pairs, S <= 8.
+__device__ __forceinline__ int ksplit_for(const LayerArgs& p, int P, int n_pairs) {
+  if (!p.ksplit_max || P == 0) return 1;
+  const int tiles = P * p.n_blocks;
+  return max(1, min(min(p.ksplit_max, p.k_blocks / 4), n_pairs / tiles));
 }
 __device__ __forceinline__ int layer0_split(int U, int n_pairs) {
   const int rem = U % n_pairs;
@@ -189,14 +199,24 @@ constexpr uint32_t kSchedReaders = 11;
 // broadcast, keeps the claim-ahead short).
 constexpr int kClaimLead = 8;
 
+// The last n-block of a layer holds <= 256 real columns.
+__device__ __forceinline__ bool narrow_block(const LayerArgs& p, int nb) {
+  const int cols = p.out_ld - nb * static_cast<int>(kBlockN);
+  return cols > 0 && cols <= static_cast<int>(kHalfN);
+}
+// 256-column halves a 128-row tile collects over all n-blocks of a layer.
+__device__ __forceinline__ uint32_t tile_halves(const LayerArgs& p) {
+  return 2u * static_cast<uint32_t>(p.n_blocks) - (narrow_block(p, p.n_blocks - 1) ? 1u : 0u);
+}
+
 __device__ __forceinline__ int seq_total(const KernelArgs& f, int P, int n_pairs, Sched& s0, Sched& s1) {
   s0 = {0, 0};
   s1 = {0, 0};
   if (f.mode != 1) {
     const int U0 = P * f.l[0].n_blocks;
-    s0 = make_sched(U0, f.l[0].split_tail ? layer0_split(U0, n_pairs) : 0);
+    s0 = make_sched(U0, f.l[0].split_tail ? layer0_split(U0, n_pairs) : 0, ksplit_for(f.l[0], P, n_pairs));
   }
-  if (f.mode != 0) s1 = make_sched(P * f.l[1].n_blocks, f.l[1].split_units);
+  if (f.mode != 0) s1 = make_sched(P * f.l[1].n_blocks, f.l[1].split_units, ksplit_for(f.l[1], P, n_pairs));
   return s0.total + s1.total;
 }
 
@@ -212,14 +232,24 @@ __device__ __forceinline__ Unit unit_at(const KernelArgs& f, int g, int P, const
   const LayerArgs& p = f.l[layer];
   Unit w;
   if (g < s.full) {
-    w = decode_unit(g, layer, p.raster, P, p.n_blocks, p.order_group, p.order_group2);
-    w.half = -1;
+    // the K slices of one output tile are consecutive claims (they finish
+    // together; the last one reduces)
+    w = decode_unit(g / s.S, layer, p.raster, P, p.n_blocks, p.order_group, p.order_group2);
+    w.ks = g % s.S;
+    // a ragged last n-block of <= 256 columns (e.g. K/tp = 3200) runs as a
+    // half unit: one 256-wide UMMA instead of two over mostly padding
+    w.half = narrow_block(p, w.nb) ? 0 : -1;
   } else {
     const int v = g - s.full;
     w = decode_unit(s.full + (v >> 1), layer, p.raster, P, p.n_blocks, p.order_group, p.order_group2);
     w.half = v & 1;
+    w.ks = 0;
   }
   return w;
+}
+
+__device__ __forceinline__ int slices_of(const Unit& w, const Sched& s0, const Sched& s1) {
+  return w.layer ? s1.S : s0.S;
 }
 
 // Compute role of a 2-CTA pair: scheduler (leader warp 3) claims units and
@@ -239,6 +269,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
   uint64_t* sempty = sfull + kSchedSlots;                     // [kSchedSlots] unit id read by all
   uint64_t* sreq = sempty + kSchedSlots;                      // producer asks for the next unit
   int* sunit = reinterpret_cast<int*>(sreq + 1);              // [kSchedSlots]
+  int* sflag = sunit + kSchedSlots;                           // epilogue: split-K finisher flag
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = blockIdx.x & 1;  // rank in the 2-CTA cluster
@@ -358,15 +389,17 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         } else if (w.layer == 1 && f.mode == 2) {
           // layer1 A = H rows written by the layer0 epilogues of this launch
           const uint32_t* hc = f.h_cnt + (row0 >> 7);
-          const uint32_t target = 2u * static_cast<uint32_t>(f.l[0].n_blocks);
+          const uint32_t target = tile_halves(f.l[0]);
           while (ptx::ld_acquire_gpu(hc) < target) __nanosleep(32);
           ptx::fence_async_global();
         }
       }
       __syncwarp();
       const uint64_t t_start = ptx::globaltimer();  // load interval starts once its A rows are ready
-      const int kb_req = max(0, p.k_blocks - kClaimLead);
-      for (int kb = 0; kb < p.k_blocks; ++kb) {
+      const int S = slices_of(w, s0, s1);
+      const int kb0 = w.ks * p.k_blocks / S, kb1 = (w.ks + 1) * p.k_blocks / S;
+      const int kb_req = max(kb0, kb1 - kClaimLead);
+      for (int kb = kb0; kb < kb1; ++kb) {
         wait(empty + stage, phase ^ 1);
         if (kb == kb_req && leader && lane == 0) ptx::mbar_arrive(sreq);  // claim the next unit now
         if (lane == 0 && (p.debug & 16)) {
@@ -399,11 +432,13 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const LayerArgs& p = f.l[w.layer];
       const bool two = w.half < 0;  // both accumulator halves (else only half 0)
       const uint32_t ephase = (it & 1) ^ 1;  // previous unit's drain of each half
+      const int S = slices_of(w, s0, s1);
+      const int kb0 = w.ks * p.k_blocks / S, kb1 = (w.ks + 1) * p.k_blocks / S;
       const uint64_t t_w = ptx::globaltimer();
       wait(tempty + 0, ephase);
       ptx::tc_fence_after();
       const uint64_t t_m = ptx::globaltimer();
-      for (int kb = 0; kb < p.k_blocks; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         wait(full + stage, phase);
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + stage * kSmemStage);
@@ -414,10 +449,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (lane == 0 && !(p.debug & 8)) {
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
-            ptx::mma_bf16_2sm(tmem_base, da + 2 * k, db0 + 2 * k, kIdesc, (kb | k) != 0);
+            ptx::mma_bf16_2sm(tmem_base, da + 2 * k, db0 + 2 * k, kIdesc, (kb != kb0) || (k != 0));
         }
         __syncwarp();
-        if (kb == 0) {  // half 1 of the accumulator drains after half 0
+        if (kb == kb0) {  // half 1 of the accumulator drains after half 0
           wait(tempty + 1, ephase);
           ptx::tc_fence_after();
         }
@@ -425,10 +460,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           if (!(p.debug & 8) && two) {
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k)
-              ptx::mma_bf16_2sm(tmem_base + kHalfN, da + 2 * k, db1 + 2 * k, kIdesc, (kb | k) != 0);
+              ptx::mma_bf16_2sm(tmem_base + kHalfN, da + 2 * k, db1 + 2 * k, kIdesc, (kb != kb0) || (k != 0));
           }
           ptx::mma_commit_2sm(empty + stage, 0x3);
-          if (kb == p.k_blocks - 1) ptx::mma_commit_2sm(tfull, 0x3);
+          if (kb == kb1 - 1) ptx::mma_commit_2sm(tfull, 0x3);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -474,51 +509,24 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           fold_t = widx / p.topk;
           fold_s = widx - fold_t * p.topk;
           if (p.combine_w) scale = p.combine_w[widx];
-          // earlier hosted rows live in units claimed before this one (same
-          // n-block columns, lower sequence index): wait for their tiles
-          for (int s2 = 0; s2 < fold_s; ++s2) {
-            const int pos = p.tok_pos[fold_t * p.topk + s2];
-            if (pos < 0) continue;
-            for (int h = h_lo; h <= h_hi; ++h) {
-              const uint32_t* fl = p.tile_done + (static_cast<long long>(pos >> 7) * NB + w.nb) * 2 + h;
-              while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(64);
-            }
-          }
         }
       }
+      // earlier hosted rows live in units claimed before this one (same
+      // n-block columns, lower sequence index): wait for their tiles
+      auto fold_wait = [&]() {
+        for (int s2 = 0; s2 < fold_s; ++s2) {
+          const int pos = p.tok_pos[fold_t * p.topk + s2];
+          if (pos < 0) continue;
+          for (int h = h_lo; h <= h_hi; ++h) {
+            const uint32_t* fl = p.tile_done + (static_cast<long long>(pos >> 7) * NB + w.nb) * 2 + h;
+            while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(64);
+          }
+        }
+      };
       const unsigned long long my_addr = reinterpret_cast<unsigned long long>(my_dst);
-#pragma unroll 1
-      for (int s = 0; s < n_chunks; ++s) {
-        const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
-        if (p.debug & 128) {  // debug: drain nothing
-          if (half_end) {
-            ptx::tc_fence_before();
-            if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
-            else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
-            if (w.half >= 0) {
-              if (leader) ptx::mbar_arrive(tempty + 1);
-              else ptx::mbar_arrive_cluster(tempty + 1, 0);
-            }
-          }
-          continue;
-        }
-        uint32_t v0[32], v1[32];
-        ptx::tmem_ld32(taddr + s * 64, v0);
-        ptx::tmem_ld32(taddr + s * 64 + 32, v1);
-        ptx::tmem_ld_wait();
-        if (half_end) {
-          // accumulator half drained: the next unit's MMAs may overwrite it
-          // (a half unit used only half 0: release both)
-          ptx::tc_fence_before();
-          const int h = s * 64 >= static_cast<int>(kHalfN);
-          if (leader) ptx::mbar_arrive(tempty + h);
-          else ptx::mbar_arrive_cluster(tempty + h, 0);
-          if (w.half >= 0) {
-            if (leader) ptx::mbar_arrive(tempty + 1);
-            else ptx::mbar_arrive_cluster(tempty + 1, 0);
-          }
-        }
-        if (s * 64 >= cols_left || (p.debug & 64)) continue;
+      // 64 fp32 columns of this lane's row -> (fold) -> activation -> bf16 ->
+      // coalesced stores
+      auto process = [&](int s, uint32_t (&v0)[32], uint32_t (&v1)[32]) {
         if (w.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -563,14 +571,102 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           else ptx::st_v4_cs(rp + s * 64 + gsub * 8, v);
         }
         __syncwarp();
+      };
+      // split-K: this slice's fp32 partial of the lane's row (128 x 512 per CTA tile)
+      const int S = slices_of(w, s0, s1);
+      const long long split_tile = static_cast<long long>(row0 >> 7) * NB + w.nb;
+      float* part_row = S > 1 ? p.part + ((split_tile * S + w.ks) * kTileRows + ew * 32 + lane) * kBlockN : nullptr;
+      if (S == 1) fold_wait();
+#pragma unroll 1
+      for (int s = 0; s < n_chunks; ++s) {
+        const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
+        if (p.debug & 128) {  // debug: drain nothing
+          if (half_end) {
+            ptx::tc_fence_before();
+            if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
+            else ptx::mbar_arrive_cluster(tempty + (s * 64 >= static_cast<int>(kHalfN)), 0);
+            if (w.half >= 0) {
+              if (leader) ptx::mbar_arrive(tempty + 1);
+              else ptx::mbar_arrive_cluster(tempty + 1, 0);
+            }
+          }
+          continue;
+        }
+        uint32_t v0[32], v1[32];
+        ptx::tmem_ld32(taddr + s * 64, v0);
+        ptx::tmem_ld32(taddr + s * 64 + 32, v1);
+        ptx::tmem_ld_wait();
+        if (half_end) {
+          // accumulator half drained: the next unit's MMAs may overwrite it
+          // (a half unit used only half 0: release both)
+          ptx::tc_fence_before();
+          const int h = s * 64 >= static_cast<int>(kHalfN);
+          if (leader) ptx::mbar_arrive(tempty + h);
+          else ptx::mbar_arrive_cluster(tempty + h, 0);
+          if (w.half >= 0) {
+            if (leader) ptx::mbar_arrive(tempty + 1);
+            else ptx::mbar_arrive_cluster(tempty + 1, 0);
+          }
+        }
+        if (S > 1) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            reinterpret_cast<uint4*>(part_row + s * 64)[i] = make_uint4(v0[4 * i], v0[4 * i + 1], v0[4 * i + 2], v0[4 * i + 3]);
+            reinterpret_cast<uint4*>(part_row + s * 64 + 32)[i] =
+                make_uint4(v1[4 * i], v1[4 * i + 1], v1[4 * i + 2], v1[4 * i + 3]);
+          }
+          continue;
+        }
+        if (s * 64 >= cols_left || (p.debug & 64)) continue;
+        process(s, v0, v1);
       }
-      const uint32_t amount = w.half < 0 ? 2u : 1u;  // completion counted in 256-column halves
+      bool finisher = true;  // this CTA produces the tile's output (always, without split-K)
+      if (S > 1) {
+        // the last slice to land reduces all S partials in slice order
+        // (deterministic) and runs the epilogue proper
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (threadIdx.x == kEpiThread0) *sflag = atomicAdd(p.split_cnt + split_tile, 1u) == static_cast<uint32_t>(S - 1);
+        ptx::named_bar_sync(1, 128);
+        finisher = *reinterpret_cast<volatile int*>(sflag) != 0;
+        if (finisher) {
+          __threadfence();
+          fold_wait();
+          const float* rows0 = p.part + (split_tile * S * kTileRows + ew * 32 + lane) * kBlockN;
+#pragma unroll 1
+          for (int s = 0; s < n_chunks; ++s) {
+            if (s * 64 >= cols_left || (p.debug & 64)) continue;
+            uint32_t v0[32], v1[32];
+            float acc[64];
+#pragma unroll
+            for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+            for (int k = 0; k < S; ++k) {
+              const float4* src = reinterpret_cast<const float4*>(rows0 + static_cast<long long>(k) * kTileRows * kBlockN + s * 64);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float4 q4 = __ldcg(src + i);
+                acc[4 * i] += q4.x; acc[4 * i + 1] += q4.y; acc[4 * i + 2] += q4.z; acc[4 * i + 3] += q4.w;
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              v0[i] = __float_as_uint(acc[i]);
+              v1[i] = __float_as_uint(acc[32 + i]);
+            }
+            process(s, v0, v1);
+          }
+          if (threadIdx.x == kEpiThread0) p.split_cnt[split_tile] = 0u;  // ready for the next launch
+        }
+      }
+      // completion counted in real 256-column halves (half 1 of a narrow last
+      // block -- a split-tail half -- covers none); split-K: by the finisher
+      const uint32_t amount = !finisher ? 0u : w.half < 0 ? 2u : ((w.half == 1 && narrow_block(p, w.nb)) ? 0u : 1u);
       if (w.layer == 0 && f.mode == 2) {
         // this CTA's 128 H rows of the unit's columns are in memory -> count
         // them for the layer1 units that read the tile as their A operand
         ptx::fence_async_global();
         ptx::named_bar_sync(1, 128);
-        if (threadIdx.x == kEpiThread0) {
+        if (threadIdx.x == kEpiThread0 && amount) {
           __threadfence();
           ptx::red_release_gpu_add(f.h_cnt + (row0 >> 7), amount);
         }
@@ -578,7 +674,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // this CTA's 128 rows of column block nb are in memory -> count them
         if (p.world > 1) __threadfence_system();  // pushed rows visible to the peer first
         ptx::named_bar_sync(1, 128);
-        if (threadIdx.x == kEpiThread0) {
+        if (threadIdx.x == kEpiThread0 && amount) {
           __threadfence();
           ptx::red_release_gpu_add(p.nb_done + w.nb, amount);
           if (p.fuse_combine)
@@ -586,7 +682,8 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
               ptx::st_release_gpu(p.tile_done + (static_cast<long long>(row0 >> 7) * NB + w.nb) * 2 + h, p.epoch);
           if (p.world > 1)
             comm::nb_contributed(p, w.nb, amount,
-                                 4u * static_cast<uint32_t>(P) + (gridDim.x - static_cast<uint32_t>(p.n_compute)));
+                                 (narrow_block(p, w.nb) ? 2u : 4u) * static_cast<uint32_t>(P) +
+                                     (gridDim.x - static_cast<uint32_t>(p.n_compute)));
         }
       }
       if (threadIdx.x == kEpiThread0) tl_record(p, kRoleEpilogue, it, g, t_e, ptx::globaltimer());

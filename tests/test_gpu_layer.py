@@ -216,3 +216,43 @@ def test_forward_host_pipeline(chunks):
     assert_close(out.float().numpy(), ref, what=f"forward_host chunks={chunks}")
     assert torch.equal(out, out2)
     layer.close()
+
+
+@pytest.mark.parametrize("tp,ep,n_comm1", [(1, 1, 0), (1, 1, 2), (2, 2, 0), (1, 4, 0)])
+def test_narrow_last_blocks(tp, ep, n_comm1):
+    """Ragged last n-blocks of <= 256 columns run as half units (K/tp = 640,
+    N = 640): per-tile H counters, combine-CTA and peer-flag targets count
+    halves, results match the oracle."""
+    model = ModelConfig(L=1, E=8, topk=2, N=640, K=1280)
+    par = ParallelSpec(tp, ep)
+    routing = build_routing(model, par, WorkloadSpec(M=900, seed=41, std=0.032))
+    w = random_weights(model, seed=42)
+    x = np.random.default_rng(43).standard_normal((900, 640))
+    cw = np.random.default_rng(44).random((900, 2))
+    y = run_emulated(x, w, routing, par, combine_weights=cw,
+                     knobs=LayerKnobs(n_comm0=8, n_comm1=n_comm1)).cpu().numpy()
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), combine_weights=cw, tp=tp)
+    assert_close(y, ref, what=f"narrow tp={tp} ep={ep} n_comm1={n_comm1}")
+
+
+@pytest.mark.parametrize("tp,ep,M", [(1, 8, 300), (1, 1, 200), (2, 4, 500), (1, 4, 64)])
+def test_split_k_small_m(tp, ep, M, monkeypatch):
+    """Few output tiles per rank -> split-K (fp32 partials, the last slice
+    reduces in slice order): within tolerance of the oracle, run-to-run
+    bitwise deterministic, and close to the unsplit path."""
+    model = ModelConfig(L=1, E=8, topk=2, N=512, K=2048)
+    par = ParallelSpec(tp, ep)
+    routing = build_routing(model, par, WorkloadSpec(M=M, seed=51, std=0.032))
+    w = random_weights(model, seed=52)
+    x = np.random.default_rng(53).standard_normal((M, 512))
+    cw = np.random.default_rng(54).random((M, 2))
+    ys = []
+    for ks in ("8", "8", "0"):
+        monkeypatch.setenv("COMET_KSPLIT", ks)
+        ys.append(run_emulated(x, w, routing, par, activation="gelu_tanh", combine_weights=cw,
+                               knobs=LayerKnobs(n_comm0=8, n_comm1=0)).cpu().numpy())
+    np.testing.assert_array_equal(ys[0], ys[1])
+    gelu = lambda a: 0.5 * a * (1 + np.tanh(0.7978845608028654 * (a + 0.044715 * a ** 3)))  # noqa: E731
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), gelu, cw, tp=tp)
+    assert_close(ys[0], ref, what=f"split-K tp={tp} ep={ep} M={M}")
+    assert_close(ys[2], ref, what=f"unsplit tp={tp} ep={ep} M={M}")
