@@ -572,10 +572,14 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         }
         __syncwarp();
       };
-      // split-K: this slice's fp32 partial of the lane's row (128 x 512 per CTA tile)
+      // split-K: this slice's fp32 partial of the CTA's 128 x 512 tile, stored
+      // column-quad major ([c/4][row][4]) so a warp's 32 rows of one quad are
+      // 512 contiguous bytes (coalesced stores and reloads)
       const int S = slices_of(w, s0, s1);
       const long long split_tile = static_cast<long long>(row0 >> 7) * NB + w.nb;
-      float* part_row = S > 1 ? p.part + ((split_tile * S + w.ks) * kTileRows + ew * 32 + lane) * kBlockN : nullptr;
+      float4* part_row = S > 1 ? reinterpret_cast<float4*>(p.part + (split_tile * S + w.ks) * kTileRows * kBlockN) +
+                                     ew * 32 + lane
+                               : nullptr;
       if (S == 1) fold_wait();
 #pragma unroll 1
       for (int s = 0; s < n_chunks; ++s) {
@@ -611,9 +615,11 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (S > 1) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            reinterpret_cast<uint4*>(part_row + s * 64)[i] = make_uint4(v0[4 * i], v0[4 * i + 1], v0[4 * i + 2], v0[4 * i + 3]);
-            reinterpret_cast<uint4*>(part_row + s * 64 + 32)[i] =
-                make_uint4(v1[4 * i], v1[4 * i + 1], v1[4 * i + 2], v1[4 * i + 3]);
+            part_row[(s * 16 + i) * kTileRows] = make_float4(__uint_as_float(v0[4 * i]), __uint_as_float(v0[4 * i + 1]),
+                                                             __uint_as_float(v0[4 * i + 2]), __uint_as_float(v0[4 * i + 3]));
+            part_row[(s * 16 + 8 + i) * kTileRows] =
+                make_float4(__uint_as_float(v1[4 * i]), __uint_as_float(v1[4 * i + 1]), __uint_as_float(v1[4 * i + 2]),
+                            __uint_as_float(v1[4 * i + 3]));
           }
           continue;
         }
@@ -632,7 +638,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (finisher) {
           __threadfence();
           fold_wait();
-          const float* rows0 = p.part + (split_tile * S * kTileRows + ew * 32 + lane) * kBlockN;
+          const float4* rows0 = reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + ew * 32 + lane;
 #pragma unroll 1
           for (int s = 0; s < n_chunks; ++s) {
             if (s * 64 >= cols_left || (p.debug & 64)) continue;
@@ -641,10 +647,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
 #pragma unroll
             for (int i = 0; i < 64; ++i) acc[i] = 0.f;
             for (int k = 0; k < S; ++k) {
-              const float4* src = reinterpret_cast<const float4*>(rows0 + static_cast<long long>(k) * kTileRows * kBlockN + s * 64);
+              const float4* src = rows0 + static_cast<long long>(k) * (kTileRows * kBlockN / 4) + s * 16 * kTileRows;
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float4 q4 = __ldcg(src + i);
+                const float4 q4 = __ldcg(src + i * kTileRows);
                 acc[4 * i] += q4.x; acc[4 * i + 1] += q4.y; acc[4 * i + 2] += q4.z; acc[4 * i + 3] += q4.w;
               }
             }
