@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   __shared__ int s_ws[kWarps];
   __shared__ int s_misc[8];
 
+  ptx::pdl_launch_dependents();  // the dispatch / layer kernels may launch; they wait for this grid
   const int tid = threadIdx.x;
   unsigned long long tt0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));

@@ -190,6 +190,7 @@ __device__ __forceinline__ void fold_row(uint32_t (&acc)[32], const __nv_bfloat1
 }
 
 constexpr int kSchedSlots = 2;
+constexpr int kLifeTask = (1 << 20) - 2;  // timeline task id of a CTA's lifetime record
 // Readers of each claimed unit id: leader CTA producer + MMA + 4 epilogue
 // warps, peer CTA producer + 4 epilogue warps (all arrive on the leader's
 // slot-empty barrier).
@@ -311,6 +312,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  ptx::pdl_wait();  // the prologue above overlapped the previous kernel's tail
 
   const int P = f.l[f.mode == 1 ? 1 : 0].meta[kMetaPairs];
   // pairs that compute: everything but layer1 combine CTAs (dispatch CTAs join)
@@ -711,13 +713,17 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
   __shared__ int s_last;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b = static_cast<int>(blockIdx.x);
+  const uint64_t t_entry = ptx::globaltimer();
   bool compute = true;
+  ptx::pdl_launch_dependents();  // the next kernel may start its launch / prologue
   if (f.mode == 1 && b >= f.l[1].n_compute) {
     // layer1 combine CTA (world 1, comm-CTA combine): reduces to the end
+    ptx::pdl_wait();
     if (!(f.l[1].debug & 1)) comm::combine_reduce(f.l[1], smem);
     compute = false;
   } else if (f.mode != 1 && b >= f.l[0].n_compute) {
     // layer0 dispatch CTA: pull the remote rows, then join the compute pairs
+    ptx::pdl_wait();
     if (!(f.l[0].debug & 1)) comm::dispatch_rows(f.l[0], smem);
     __syncthreads();
     comm::comm_release(f.l[0], smem);
@@ -728,6 +734,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
   // The last CTA out resets the launch's claim counter and H-tile counters
   // (nothing reads them after every CTA has left).
   __syncthreads();
+  {  // CTA lifetime (launch skew / prologue / tail): the last tmem-wait record, task kLifeTask
+    const LayerArgs& pl = f.l[f.mode == 1 ? 1 : 0];
+    if (threadIdx.x == 0) tl_record(pl, kRoleTmemWait, pl.timeline_cap - 1, kLifeTask, t_entry, ptx::globaltimer());
+  }
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(f.sched + 1, 1u) == gridDim.x - 1;
@@ -751,6 +761,8 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
 // summing (latency-bound: ~8 loads in flight per lane, whole GPU).
 __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb,
                                                              const uint32_t* cb_flag, const int32_t* experts) {
+  ptx::pdl_launch_dependents();
+  ptx::pdl_wait();
   const int NB = p.n_blocks, N = p.n_embed, K = p.topk, W = p.world;
   const int start = token_start_of(p.rank, p.M, W);
   const int n_own = token_stop_of(p.rank, p.M, W) - start;
@@ -821,6 +833,8 @@ __global__ void __launch_bounds__(256) dispatch_local_kernel(const int32_t* __re
                                                              const __nv_bfloat16* __restrict__ xs,
                                                              __nv_bfloat16* __restrict__ xg, int n_embed, int M,
                                                              int world, int rank) {
+  ptx::pdl_launch_dependents();
+  ptx::pdl_wait();
   const int rows = meta[kMetaRowsPad];
   const int vec = n_embed / 8;
   const int lane = threadIdx.x & 31;
@@ -849,6 +863,8 @@ __global__ void __launch_bounds__(256) combine_local_kernel(const int32_t* __res
                                                             const __nv_bfloat16* __restrict__ yrows,
                                                             __nv_bfloat16* __restrict__ y, int t0, int n_tok,
                                                             int topk, int n_embed) {
+  ptx::pdl_launch_dependents();
+  ptx::pdl_wait();
   const int vec = n_embed / 8;
   const long long items = static_cast<long long>(n_tok) * vec;
   for (long long it = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; it < items;

@@ -136,6 +136,12 @@ __device__ __forceinline__ void st_shared_cluster(void* local, uint32_t cta, uin
   asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(remote), "r"(v) : "memory");
 }
 
+// Programmatic dependent launch: the next kernel in the stream may start
+// (launch_dependents); block until the previous kernel finished and its
+// memory is visible (wait).  No-ops for launches without the PDL attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ TMA --
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

@@ -48,6 +48,9 @@ U0 = P * NB0
 split1 = int(os.environ.get("COMET_SPLIT1", 0))
 U1 = P * NB1
 full1 = U1 - min(U1, split1)
+LIFE = (1 << 20) - 2
+life = [x for x in recs if x[1] == "tmem_wait" and x[2] == LIFE]
+recs = [x for x in recs if not (x[1] == "tmem_wait" and x[2] == LIFE)]
 t0 = min(x[3] for x in recs)
 span = max(x[4] for x in recs) - t0
 print(f"rank0: P={P} NB0={NB0} NB1={NB1} U0={U0} U1={U1} (halves from layer1 unit {full1}); span {span/1e3:.1f} us")
@@ -69,6 +72,10 @@ for k in ("L0", "L1", "L1h"):
     d = [x[3] - x[2] for x in mma if kind(x[1]) == k]
     if d:
         print(f"  MMA {k:3s}: n={len(d):4d} mean {statistics.mean(d)/1e3:7.2f} us  min {min(d)/1e3:7.2f}  max {max(d)/1e3:7.2f}")
+    d = [(x[3] - x[2], x[3]) for x in by_role.get("epilogue", []) if kind(x[1]) == k]
+    if d:
+        print(f"  EPI {k:3s}: n={len(d):4d} mean {statistics.mean(v for v, _ in d)/1e3:7.2f} us  max {max(v for v, _ in d)/1e3:7.2f}"
+              f"  last end +{max(e for _, e in d)/1e3:7.1f}")
 # per pair (leader CTA) chronology
 pairs = {}
 for c, task, s, e in mma:
@@ -85,6 +92,10 @@ for c in sorted(pairs):
 ends.sort()
 print("pair end times (us): min %.1f median %.1f max %.1f" % (ends[0][0] / 1e3, ends[len(ends) // 2][0] / 1e3,
                                                             ends[-1][0] / 1e3))
+if life:
+    print("CTA lifetime: entry first %+.1f last %+.1f us | exit first %+.1f last %+.1f us (rel. to first record)" % (
+        (min(x[3] for x in life) - t0) / 1e3, (max(x[3] for x in life) - t0) / 1e3,
+        (min(x[4] for x in life) - t0) / 1e3, (max(x[4] for x in life) - t0) / 1e3))
 comm = by_role.get("comm", [])
 if comm:
     print(f"  dispatch: {len(comm)} tiles, last published +{max(x[3] for x in comm)/1e3:.1f} us")
