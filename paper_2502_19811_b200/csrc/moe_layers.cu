@@ -174,12 +174,11 @@ __device__ __forceinline__ void pack_chunk(const uint32_t (&v0)[32], const uint3
     pk[16 + i] = pack_bf16(activate<ACT>(__uint_as_float(v1[2 * i])), activate<ACT>(__uint_as_float(v1[2 * i + 1])));
 }
 
-// acc[0..32) += w * 32 bf16 of an earlier expert row (fused combine fold)
-__device__ __forceinline__ void fold_row(uint32_t (&acc)[32], const __nv_bfloat16* src, float w) {
+// acc[0..32) += w * 32 bf16 already in registers (r[0..4) = 4 x uint4)
+__device__ __forceinline__ void fold_regs(uint32_t (&acc)[32], const uint4* r, float w) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint4 v = *reinterpret_cast<const uint4*>(src + q * 8);  // written by this kernel: no .nc
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[q]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 f = __bfloat1622float2(h[j]);
@@ -188,6 +187,7 @@ __device__ __forceinline__ void fold_row(uint32_t (&acc)[32], const __nv_bfloat1
     }
   }
 }
+constexpr int kMaxFold = 7;  // earlier hosted rows of a token (top-k <= 8)
 
 constexpr int kSchedSlots = 2;
 constexpr int kLifeTask = (1 << 20) - 2;  // timeline task id of a CTA's lifetime record
@@ -502,6 +502,9 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN + col0;
       float scale = 1.f;
       int fold_t = -1, fold_s = 0;  // token and own slot of a last-hosted row
+      int nf = 0;                   // earlier hosted rows to fold, their rows and weights
+      int fpos[kMaxFold];
+      float fw[kMaxFold];
       if (w.layer == 1 && p.fuse_combine) {
         const int rd = p.row_dst[my_row];
         if (rd >= 0) {
@@ -511,6 +514,19 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           fold_t = widx / p.topk;
           fold_s = widx - fold_t * p.topk;
           if (p.combine_w) scale = p.combine_w[widx];
+#pragma unroll
+          for (int s2 = 0; s2 < kMaxFold; ++s2) {
+            if (s2 >= fold_s) break;
+            const int pos = p.tok_pos[fold_t * p.topk + s2];
+            if (pos < 0) continue;
+#pragma unroll
+            for (int j = 0; j < kMaxFold; ++j)  // static register indexing
+              if (j == nf) {
+                fpos[j] = pos;
+                fw[j] = p.combine_w ? p.combine_w[fold_t * p.topk + s2] : 1.f;
+              }
+            ++nf;
+          }
         }
       }
       // earlier hosted rows live in units claimed before this one (same
@@ -535,14 +551,28 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
             v0[i] = __float_as_uint(__uint_as_float(v0[i]) * scale);
             v1[i] = __float_as_uint(__uint_as_float(v1[i]) * scale);
           }
-          for (int s2 = 0; s2 < fold_s; ++s2) {
-            const int pos = p.tok_pos[fold_t * p.topk + s2];
-            if (pos < 0) continue;
-            const float ws = p.combine_w ? p.combine_w[fold_t * p.topk + s2] : 1.f;
-            const __nv_bfloat16* src =
-                p.yrows + static_cast<long long>(pos) * p.n_embed + w.nb * kBlockN + col0 + s * 64;
-            fold_row(v0, src, ws);
-            fold_row(v1, src + 32, ws);
+          // earlier hosted rows, ascending slot: two rows' loads in flight per
+          // round trip (a serial load->fma chain made top-8 epilogues ~100 us)
+#pragma unroll
+          for (int j = 0; j < kMaxFold; j += 2) {
+            if (j >= nf) break;
+            uint4 ra[8], rb[8];
+            const __nv_bfloat16* a = p.yrows + static_cast<long long>(fpos[j]) * p.n_embed + w.nb * kBlockN + col0 + s * 64;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ra[q] = *reinterpret_cast<const uint4*>(a + q * 8);
+            const bool two = j + 1 < nf && j + 1 < kMaxFold;
+            if (two) {
+              const __nv_bfloat16* b =
+                  p.yrows + static_cast<long long>(fpos[j + 1 < kMaxFold ? j + 1 : j]) * p.n_embed + w.nb * kBlockN + col0 + s * 64;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) rb[q] = *reinterpret_cast<const uint4*>(b + q * 8);
+            }
+            fold_regs(v0, ra, fw[j]);
+            fold_regs(v1, ra + 4, fw[j]);
+            if (two) {
+              fold_regs(v0, rb, fw[j + 1 < kMaxFold ? j + 1 : j]);
+              fold_regs(v1, rb + 4, fw[j + 1 < kMaxFold ? j + 1 : j]);
+            }
           }
         }
         uint32_t pk[32];
