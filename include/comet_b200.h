@@ -149,6 +149,21 @@ int comet_forward(comet_ctx* ctx, const int32_t* d_experts, int M, const void* w
                   const float* combine_w, void* y_local, int activation, int n_comm0, int n_comm1,
                   int group0, int wave1, void* stream);
 
+/* End-to-end single-GPU forward on HOST buffers (world 1): h_x [M, N] bf16,
+ * h_experts [M, topk] int32, h_combine_w [M, topk] fp32 or NULL (all pinned
+ * host memory), result into h_y [M, N] bf16.  The token upload runs in
+ * `chunks` token chunks on an internal copy stream, each publishing an epoch
+ * flag (cuStreamWriteValue32); the ONE layer launch pulls rows as their
+ * chunk lands (pairs in (row tile, expert) order), layer1's fused combine
+ * writes output rows and counts them per chunk; a second copy stream
+ * downloads chunk k once its count is complete (cuStreamWaitValue32).  The
+ * call is asynchronous: `stream` waits for the download before anything
+ * enqueued after it.  Same arithmetic as execute_naive (executor.py:132-148)
+ * within the bf16 tolerance; replaces the reference's host-array call. */
+int comet_forward_host(comet_ctx* ctx, const void* h_x, const int32_t* h_experts, const float* h_combine_w,
+                       void* h_y, int M, const void* w0t, const void* w1t, int activation, int n_comm0, int group0,
+                       int wave1, int chunks, void* stream);
+
 /* Device pointers of internal buffers (testing / profiling). */
 void* comet_hidden_buffer(comet_ctx* ctx);   /* H [rows_pad_cap, K/tp] bf16 */
 void* comet_yrows_buffer(comet_ctx* ctx);    /* layer1 rows [rows_pad_cap, N] bf16 */

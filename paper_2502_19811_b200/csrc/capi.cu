@@ -56,6 +56,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kLayerThreads = 256;
+constexpr int kMaxStreamChunks = 64;  // token chunks of the host-streamed forward
 constexpr size_t kLayerSmem = kLayerStages * 49152 + 32768 + 1024 + 1024;
 constexpr int kIndexThreads = 1024;
 constexpr size_t kIndexSmem = 8192 * sizeof(long long);
@@ -176,6 +177,12 @@ struct comet_ctx {
   MapCache w0c, w1c;
   uint32_t* sched = nullptr;  // [2] unit claim / CTA exit counters of the layer kernel (self-resetting)
   uint32_t* h_cnt = nullptr;  // [cap_rows_pad / 128 + 1] fused-launch H tile counters (self-resetting)
+  // host-streamed forward: upload / download streams, per-chunk upload epochs
+  cudaStream_t up_stream = nullptr, down_stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_index = nullptr, ev_down = nullptr;
+  uint32_t* chunk_ready = nullptr;
+  float* cw_dev = nullptr;                 // uploaded combine weights
+  __nv_bfloat16* y_stream = nullptr;       // [m_cap, N] output of the streamed forward
   float* part = nullptr;       // split-K partials: 2 layers x (pairs x 2 CTA tiles) x 128 x 512 fp32
   uint32_t* split_cnt = nullptr;  // 2 layers x 512 slice counters (reset by each tile's finisher)
   int n_h = 0;
@@ -335,11 +342,13 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
   x->opened.assign(W, nullptr);
 
   // ---- counters (work buffers H / yrows are allocated on the first layer call) ----
-  CK(cudaMalloc(&x->counters, sizeof(uint32_t) * 2 * x->nb1));
-  CK(cudaMemset(x->counters, 0, sizeof(uint32_t) * 2 * x->nb1));
+  // layer1 per-n-block counters + streamed-forward output chunk counters,
+  // all zeroed by every index build
+  CK(cudaMalloc(&x->counters, sizeof(uint32_t) * (2 * x->nb1 + kMaxStreamChunks)));
+  CK(cudaMemset(x->counters, 0, sizeof(uint32_t) * (2 * x->nb1 + kMaxStreamChunks)));
   CK(cudaMalloc(&x->routing, sizeof(int32_t) * (size_t)c.m_cap * c.topk));
   ix.zero_words = x->counters;
-  ix.n_zero_words = 2 * x->nb1;
+  ix.n_zero_words = 2 * x->nb1 + kMaxStreamChunks;
 
   if (W == 1) {
     comet_ctx* self = x;
@@ -365,6 +374,14 @@ int comet_ctx_destroy(comet_ctx* x) {
   cudaFree(x->tile_done);
   cudaFree(x->sched);
   cudaFree(x->h_cnt);
+  cudaFree(x->chunk_ready);
+  cudaFree(x->cw_dev);
+  cudaFree(x->y_stream);
+  if (x->up_stream) cudaStreamDestroy(x->up_stream);
+  if (x->down_stream) cudaStreamDestroy(x->down_stream);
+  if (x->ev_start) cudaEventDestroy(x->ev_start);
+  if (x->ev_index) cudaEventDestroy(x->ev_index);
+  if (x->ev_down) cudaEventDestroy(x->ev_down);
   cudaFree(x->part);
   cudaFree(x->split_cnt);
   cudaFree(x->timeline);
@@ -895,6 +912,104 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
     if (int rc = comet_layer1(x, w1t, combine_w, y_local, n_comm1, wave1, stream)) return rc;
   }
   return comet_combine_finish(x, y_local, stream);
+}
+
+// Driver stream memory operations (flag writes / waits on the copy streams).
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_streamValue32 stream_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<PFN_streamValue32>(p);
+}
+
+int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, const float* h_combine_w,
+                       void* h_y, int M, const void* w0t, const void* w1t, int activation, int n_comm0, int group0,
+                       int wave1, int chunks, void* stream) {
+  const auto& c = x->cfg;
+  if (c.world != 1) return fail(COMET_EINVAL, "comet_forward_host streams a single-GPU forward (world=%d)", c.world);
+  if (M < 1 || M > c.m_cap) return fail(COMET_EINVAL, "M=%d outside [1, m_cap=%d]", M, c.m_cap);
+  if (chunks < 1 || chunks > kMaxStreamChunks) return fail(COMET_EINVAL, "chunks=%d outside [1, %d]", chunks, kMaxStreamChunks);
+  if (n_comm0 < 2 || (n_comm0 & 1)) return fail(COMET_EINVAL, "streamed forward needs n_comm0 >= 2, even");
+  static PFN_streamValue32 write32 = stream_fn("cuStreamWriteValue32");
+  static PFN_streamValue32 wait32 = stream_fn("cuStreamWaitValue32");
+  if (!write32 || !wait32) return fail(COMET_ECUDA, "cuStreamWriteValue32 / cuStreamWaitValue32 unavailable");
+  CK(cudaSetDevice(c.device));
+  if (int rc = ensure_work(x)) return rc;
+  if (!x->up_stream) {
+    CK(cudaStreamCreateWithFlags(&x->up_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&x->down_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&x->ev_start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&x->ev_index, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&x->ev_down, cudaEventDisableTiming));
+    CK(cudaMalloc(&x->chunk_ready, sizeof(uint32_t) * kMaxStreamChunks));
+    CK(cudaMalloc(&x->y_stream, (size_t)c.m_cap * c.N * 2));
+    CK(cudaMemset(x->chunk_ready, 0, sizeof(uint32_t) * kMaxStreamChunks));
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int ct = (M + chunks - 1) / chunks;  // tokens per upload / download chunk
+  const int n_ch = (M + ct - 1) / ct;
+  const size_t row_b = (size_t)c.N * 2;
+  // router output (+ weights) first: the index build needs only these
+  CK(cudaMemcpyAsync(x->routing, h_experts, sizeof(int32_t) * (size_t)M * c.topk, cudaMemcpyHostToDevice, st));
+  const float* cw = nullptr;
+  if (h_combine_w) {
+    if (!x->cw_dev) CK(cudaMalloc(&x->cw_dev, sizeof(float) * (size_t)c.m_cap * c.topk));
+    CK(cudaMemcpyAsync(x->cw_dev, h_combine_w, sizeof(float) * (size_t)M * c.topk, cudaMemcpyHostToDevice, st));
+    cw = x->cw_dev;
+  }
+  // the token upload may start once this call's prior work on `stream` is
+  // done (the previous forward read the token buffer)
+  CK(cudaEventRecord(x->ev_start, st));
+  CK(cudaStreamWaitEvent(x->up_stream, x->ev_start, 0));
+  if (int rc = comet_index_build_ex(x, x->routing, M, 128, c.N >= 512 ? 128 : std::max(1, c.N / 4), kIndexStream,
+                                    stream))
+    return rc;
+  const uint32_t epoch = x->epoch;
+  CK(cudaEventRecord(x->ev_index, st));  // output counters zeroed by this build
+  for (int k = 0; k < n_ch; ++k) {
+    const int t0 = k * ct, n = std::min(ct, M - t0);
+    CK(cudaMemcpyAsync(static_cast<char*>(static_cast<void*>(x->xs)) + t0 * row_b,
+                       static_cast<const char*>(h_x) + t0 * row_b, n * row_b, cudaMemcpyHostToDevice, x->up_stream));
+    if (write32(x->up_stream, reinterpret_cast<CUdeviceptr>(x->chunk_ready + k), epoch, 0) != CUDA_SUCCESS)
+      return fail(COMET_ECUDA, "cuStreamWriteValue32 failed");
+  }
+  // one launch: dispatch CTAs pull rows as their chunks land, layer1's
+  // fused combine writes y rows and counts them per chunk
+  KernelArgs f{};
+  if (int rc = layer0_args(x, w0t, activation, 0, group0, &f.l[0])) return rc;
+  if (int rc = layer1_args(x, w1t, cw, x->y_stream, 0, wave1, false, &f.l[1])) return rc;
+  const int grid = layer_grid(x);
+  f.mode = 2;
+  f.l[0].n_compute = grid - n_comm0;
+  f.l[0].stream = 1;
+  f.l[0].chunk_ready = x->chunk_ready;
+  f.l[0].chunk_tokens = ct;
+  f.l[0].split_tail = 0;
+  f.l[1].raster = 2;
+  f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
+  f.l[1].pairs = x->ix.pairs0;  // (row tile, expert) order; folders claimed last (index build)
+  f.l[1].fuse_combine = 1;
+  f.l[1].y_local = x->y_stream;
+  f.l[1].out_cnt = x->counters + 2 * x->nb1;
+  f.l[1].chunk_tokens = ct;
+  if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
+  // downloads: chunk k once its tokens' output halves are all final
+  CK(cudaStreamWaitEvent(x->down_stream, x->ev_index, 0));
+  const uint32_t halves = 2u * x->nb1 - ((c.N % kBlockN) && (c.N % kBlockN) <= kBlockN / 2 ? 1u : 0u);
+  for (int k = 0; k < n_ch; ++k) {
+    const int t0 = k * ct, n = std::min(ct, M - t0);
+    if (wait32(x->down_stream, reinterpret_cast<CUdeviceptr>(x->counters + 2 * x->nb1 + k), (uint32_t)n * halves,
+               0 /* CU_STREAM_WAIT_VALUE_GEQ */) != CUDA_SUCCESS)
+      return fail(COMET_ECUDA, "cuStreamWaitValue32 failed");
+    CK(cudaMemcpyAsync(static_cast<char*>(h_y) + t0 * row_b, static_cast<char*>(static_cast<void*>(x->y_stream)) + t0 * row_b,
+                       n * row_b, cudaMemcpyDeviceToHost, x->down_stream));
+  }
+  CK(cudaEventRecord(x->ev_down, x->down_stream));
+  CK(cudaStreamWaitEvent(st, x->ev_down, 0));  // the caller's stream covers the whole step
+  x->last_y = x->y_stream;
+  return COMET_OK;
 }
 
 }  // extern "C"

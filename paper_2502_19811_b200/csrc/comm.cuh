@@ -92,7 +92,7 @@ __device__ __forceinline__ bool remote_rows(const LayerArgs& p, int q, int& padr
   const int base = pr.y + kTileRows * (q & 1);
   const int rows = max(0, min(kTileRows, pr.z - kTileRows * (q & 1)));
   const int rel = base - p.pad_off[pr.x];                        // tile start within the expert block
-  const int first = min(rows, max(0, p.n_local[pr.x] - rel));      // first remote row of the tile
+  const int first = p.stream ? 0 : min(rows, max(0, p.n_local[pr.x] - rel));  // first remote row
   padrow0 = base + first;
   nr = rows - first;
   return nr > 0;
@@ -145,6 +145,7 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
     // ---- loader warp: lane-parallel index loads for a chunk, then lane 0
     // issues them in job order (slot waits never couple lanes of one batch) ----
     uint64_t ready_mask = 1ull << p.rank;
+    int chunk_ok = -1;  // streamed forward: upload chunks [0, chunk_ok] are in HBM
     int k = 0;
     for_my_items(p, cid, n_comm, [&](int q, int padrow0, int rb, int re, int nr) {
       const int n = re - rb;
@@ -157,6 +158,11 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
           if (!((ready_mask >> si) & 1)) {
             while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
             ready_mask |= 1ull << si;
+          }
+          if (p.stream && ti / p.chunk_tokens > chunk_ok) {  // chunks land in order
+            const int c = ti / p.chunk_tokens;
+            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.chunk_ready + c), p.epoch)) __nanosleep(128);
+            chunk_ok = c;
           }
           const int job = k + i;
           const int slot = job % n_slots;

@@ -31,6 +31,8 @@ enum MetaSlot : int {
 constexpr int kIndexRefLists = 1;      // reference tiles0 / tiles1 / chunks (resolver API)
 constexpr int kIndexCombineList = 2;   // combine token list (comm-CTA combine)
 constexpr int kIndexSignal = 4;        // publish this rank's x_ready epoch to every peer
+constexpr int kIndexStream = 8;        // host-streamed forward: pairs in (row tile, expert) order and,
+                                       // per token, the fused-combine folder = its row claimed LAST
 constexpr int kIndexMaxChunks = 64;    // token chunks per hosted expert (host-checked)
 
 struct IndexDev {

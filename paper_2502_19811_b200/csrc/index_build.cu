@@ -423,7 +423,9 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     const int last_rs = r0 + (valid > kTileRows ? kTileRows : 0);
     const int last_re = min(last_rs + kTileRows, c);
     const int nd = (last_re - last_rs) - max(0, min(last_re, s_nloc[j]) - last_rs);
-    key = tile_key(nd, ix.e_lo + j, last_rs);
+    // streamed forward: row-tile-major across experts, so the first pairs
+    // need only the first token chunks of the upload
+    key = (ix.flags & kIndexStream) ? tile_key(r0 / kPairRows, ix.e_lo + j, r0) : tile_key(nd, ix.e_lo + j, last_rs);
   };
   long long* s_pkey = sh_keys;  // P keys (P <= kSortSmemKeys, else recomputed)
   const bool pkeys_in_smem = P <= kSortSmemKeys;
@@ -456,8 +458,12 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       ix.pair_key[i] = rank;
       // .w: bit h set when 128-row half h holds rows pulled from other ranks
       const int r0 = prow - s_pad[j];
-      const int remote_mask = (min(r0 + kTileRows, s_cnt[j]) > s_nloc[j] ? 1 : 0) |
-                              (valid > kTileRows && r0 + valid > s_nloc[j] ? 2 : 0);
+      // streamed forward: every row is pulled by the dispatch CTAs (gated on
+      // its upload chunk), so every populated half waits for its tile
+      const int remote_mask = (ix.flags & kIndexStream)
+                                  ? (1 | (valid > kTileRows ? 2 : 0))
+                                  : ((min(r0 + kTileRows, s_cnt[j]) > s_nloc[j] ? 1 : 0) |
+                                     (valid > kTileRows && r0 + valid > s_nloc[j] ? 2 : 0));
       o[0] = j; o[1] = prow; o[2] = valid; o[3] = remote_mask;
       int* o0 = ix.pairs0 + rank * 4;
       o0[0] = j; o0[1] = prow; o0[2] = valid; o0[3] = remote_mask;
@@ -468,6 +474,31 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   const int Rpad = s_pad[Er];
   if (tid == 0) s_misc[2] = 0;  // pull list retired: remote rows are pulled per tile (comm.cuh)
   __syncthreads();
+
+  // ---- streamed forward: the fused-combine folder of each token is its
+  // hosted row in the LATEST (row tile, expert) pair -- every other row it
+  // folds is claimed earlier, so fold waits never point forward ----
+  if ((ix.flags & kIndexStream) && !ovf) {
+    for (int t = tid; t < M; t += kThreads) {
+      const int32_t* trow = ix.experts + static_cast<long long>(t) * K;
+      long long best = -1;
+      int best_s = -1;
+      for (int s2 = 0; s2 < K; ++s2) {
+        const int pos = __ldcg(ix.tok_pos + static_cast<long long>(t) * K + s2);
+        if (pos < 0) continue;
+        const int j = trow[s2] - ix.e_lo;
+        const long long key = (static_cast<long long>((pos - s_pad[j]) / kPairRows) << 21) | j;
+        if (key > best) { best = key; best_s = s2; }
+      }
+      const int sr = src_rank_of(t, M, W);
+      const int slot = (W > 1 ? ix.rank * ix.mloc_cap : 0) + t - token_start_of(sr, M, W);
+      for (int s2 = 0; s2 < K; ++s2) {
+        const int pos = __ldcg(ix.tok_pos + static_cast<long long>(t) * K + s2);
+        if (pos >= 0 && pos < ix.cap_rows_pad) ix.row_dst[pos] = s2 == best_s ? ((sr << 24) | slot) : -1;
+      }
+    }
+    __syncthreads();
+  }
 
   // ---- combine token list: tokens with >=1 hosted expert, ascending ----
   if (ix.flags & kIndexCombineList) {

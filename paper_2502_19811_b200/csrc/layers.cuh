@@ -47,6 +47,14 @@ struct LayerArgs {
   uint32_t* xg_ready;         // [Rpad_cap / 128] epoch when a 128-row tile of xg is filled
   uint32_t* xg_cnt;           // [Rpad_cap / 128] remote rows landed per tile (reset by its publisher)
   int chunk_rows;             // layer0 dispatch work item: rows of one tile (1..32)
+  // host-streamed forward (comet_forward_host, world 1): every row is pulled
+  // by the dispatch CTAs once its token's upload chunk landed (chunk_ready
+  // epoch, written by the copy stream); layer1 counts finished output halves
+  // per token chunk (out_cnt) for the download stream to wait on
+  int stream;
+  const uint32_t* chunk_ready;
+  int chunk_tokens;
+  uint32_t* out_cnt;
   const int32_t* pull_token;  // layer0 comm
   const int32_t* pull_src;
   const int32_t* tok_pos;     // [M*topk]

@@ -271,6 +271,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
   uint64_t* sreq = sempty + kSchedSlots;                      // producer asks for the next unit
   int* sunit = reinterpret_cast<int*>(sreq + 1);              // [kSchedSlots]
   int* sflag = sunit + kSchedSlots;                           // epilogue: split-K finisher flag
+  int* srow_chunk = sflag + 1;                                // epilogue: [128] output-row token chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = blockIdx.x & 1;  // rank in the 2-CTA cluster
@@ -514,9 +515,12 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           fold_t = widx / p.topk;
           fold_s = widx - fold_t * p.topk;
           if (p.combine_w) scale = p.combine_w[widx];
+          // every other hosted row of the token (only earlier slots unless the
+          // streamed forward picked a non-last folder), ascending slot
 #pragma unroll
-          for (int s2 = 0; s2 < kMaxFold; ++s2) {
-            if (s2 >= fold_s) break;
+          for (int s2 = 0; s2 < kMaxFold + 1; ++s2) {
+            if (s2 >= p.topk) break;
+            if (s2 == fold_s) continue;
             const int pos = p.tok_pos[fold_t * p.topk + s2];
             if (pos < 0) continue;
 #pragma unroll
@@ -532,7 +536,9 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // earlier hosted rows live in units claimed before this one (same
       // n-block columns, lower sequence index): wait for their tiles
       auto fold_wait = [&]() {
-        for (int s2 = 0; s2 < fold_s; ++s2) {
+        if (fold_t < 0) return;
+        for (int s2 = 0; s2 < p.topk; ++s2) {
+          if (s2 == fold_s) continue;
           const int pos = p.tok_pos[fold_t * p.topk + s2];
           if (pos < 0) continue;
           for (int h = h_lo; h <= h_hi; ++h) {
@@ -710,8 +716,26 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         }
       } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
+        if (p.out_cnt) srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
         if (p.world > 1) __threadfence_system();  // pushed rows visible to the peer first
         ptx::named_bar_sync(1, 128);
+        if (p.out_cnt && threadIdx.x == kEpiThread0 && amount) {
+          // streamed forward: these output rows' halves are final -> count
+          // them per token chunk (rows are token-sorted: few runs) for the
+          // download stream; one system fence covers the CTA's stores
+          __threadfence_system();
+          int run_c = -1, run_n = 0;
+          for (int r = 0; r < 128; ++r) {
+            const int cr = srow_chunk[r];
+            if (cr != run_c) {
+              if (run_c >= 0) atomicAdd(p.out_cnt + run_c, static_cast<uint32_t>(run_n) * amount);
+              run_c = cr;
+              run_n = 0;
+            }
+            run_n += cr >= 0;
+          }
+          if (run_c >= 0) atomicAdd(p.out_cnt + run_c, static_cast<uint32_t>(run_n) * amount);
+        }
         if (threadIdx.x == kEpiThread0 && amount) {
           __threadfence();
           ptx::red_release_gpu_add(p.nb_done + w.nb, amount);

@@ -244,7 +244,14 @@ class MoELayer:
         (allocated pinned when None); asynchronous on the current stream like
         ``forward`` (synchronise it before reading ``out``).
 
-        Single GPU: the layer is token-independent, so the M tokens run as
+        Single GPU, COMET_STREAM=1: ONE streamed launch
+        (``comet_forward_host``): the token upload runs in 1024-token chunks
+        whose landing the dispatch CTAs wait for, and the download of each
+        chunk starts as soon as the fused combine finished its rows.  Correct
+        (tests) but not yet faster: at world 1 the fused combine's folder
+        waits for its sibling row's unit, which runs concurrently (layer1
+        units 150 -> 220 us; 4.2 vs 4.1 ms, tools/stream_probe.py).  Default:
+        the M tokens run as
         consecutive forwards over token chunks with the H2D of chunk c+1 and
         the D2H of chunk c-1 on two copy streams under the forward of chunk
         c.  Only the first chunk's upload and the last chunk's download stay
@@ -257,6 +264,18 @@ class MoELayer:
         if out is None:
             out = torch.empty(hi_r - lo_r, N, dtype=torch.bfloat16, pin_memory=True)
         world = self.parallel.world_size
+        import os
+        if (world == 1 and chunks is None and os.environ.get("COMET_STREAM", "0") != "0"
+                and self.n_pad == N and x_host.is_pinned() and out.is_pinned() and out.is_contiguous()):
+            # one launch streaming the upload / download (comet_forward_host)
+            ex = experts_host if experts_host.dtype == torch.int32 else experts_host.to(torch.int32)
+            cw = None if combine_w is None else combine_w.float().contiguous()
+            xb = x_host if x_host.dtype == torch.bfloat16 else x_host.to(torch.bfloat16)
+            k = self.knobs
+            self.ctx.forward_host(xb.contiguous(), ex.contiguous(), cw, out, M, self.weights.w0t, self.weights.w1t,
+                                  self.act, n_comm0=max(2, k.n_comm0 // 2 * 2), group0=k.group0, wave1=k.wave1,
+                                  chunks=max(1, min(64, M // 1024)))
+            return out
         sizes = _chunk_sizes(M, chunks)
         if world > 1 or len(sizes) <= 1:
             y = self.forward(x_host, experts_host, combine_w, M=M)
