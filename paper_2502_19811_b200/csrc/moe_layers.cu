@@ -717,7 +717,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
         if (p.out_cnt) srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
-        if (p.world > 1) __threadfence_system();  // pushed rows visible to the peer first
+        // pushed rows become visible to the peer through the releasing
+        // thread's system-scope fence in nb_contributed (cumulative over the
+        // CTA's stores ordered before it by the barrier) -- one fence per CTA
+        // instead of one per thread
         ptx::named_bar_sync(1, 128);
         if (p.out_cnt && threadIdx.x == kEpiThread0 && amount) {
           // streamed forward: these output rows' halves are final -> count
