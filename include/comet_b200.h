@@ -103,9 +103,11 @@ void* comet_routing_buffer(comet_ctx* ctx);
 int comet_index_build(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_rows, int tile_cols,
                       void* stream);
 /* Same, choosing what is emitted besides the kernels' work tables:
- * flags bit0 = reference tile lists (tiles0/tiles1/chunks), bit1 = combine
- * token list (needed by comm-CTA combine).  comet_index_build = flags 3;
- * comet_forward builds only what its kernels consume. */
+ * flags bit0 = reference outputs (tiles0/tiles1/chunks and the global
+ * counts / transfer matrix), bit1 = combine token list (needed by comm-CTA
+ * combine), bit2 = publish this rank's token-ready epoch to the peers, bit3 =
+ * streamed-forward pair order.  comet_index_build = flags 3; comet_forward
+ * builds only what its kernels consume (counts / transfer are then stale). */
 int comet_index_build_ex(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_rows, int tile_cols,
                          int flags, void* stream);
 /* Sizes of the index arrays after a build (synchronises the stream). */

@@ -538,7 +538,7 @@ int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile
   }
   // global histogram + transfer matrix accumulate by atomics: zero both (adjacent)
   const size_t zbytes = reinterpret_cast<char*>(x->ix.transfer + c.world * c.world) - reinterpret_cast<char*>(x->ix.counts);
-  CK(cudaMemsetAsync(x->ix.counts, 0, zbytes, static_cast<cudaStream_t>(stream)));
+  if (flags & kIndexRefLists) CK(cudaMemsetAsync(x->ix.counts, 0, zbytes, static_cast<cudaStream_t>(stream)));
   index_build_kernel<<<grid, kIndexThreads, kIndexSmem, static_cast<cudaStream_t>(stream)>>>(ix);
   CK(cudaGetLastError());
   x->ix.experts = d_experts;  // the layer1 finish kernel reads the global routing
@@ -843,7 +843,11 @@ int comet_layers(comet_ctx* x, const void* w0t, const void* w1t, const float* co
   f.l[0].split_tail = env_int("COMET_SPLIT0", 1) != 0;
   if (!f.l[1].fuse_combine || x->E_r == 1 || x->cfg.topk == 1) f.l[1].pairs = x->ix.pairs0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (int rc = dispatch_local(x, st)) return rc;
+  // world > 1: the dispatch CTAs place the local rows too (locality-first:
+  // they are the first tiles claimed), saving the local-dispatch launch
+  f.l[0].pull_local = x->cfg.world > 1 && env_int("COMET_PULL_LOCAL", 1) != 0;
+  if (!f.l[0].pull_local)
+    if (int rc = dispatch_local(x, st)) return rc;
   if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
   if (int rc = local_combine(x, f.l[1], combine_w, y_local, st)) return rc;
   x->last_y = y_local;
@@ -984,6 +988,7 @@ int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, 
   f.mode = 2;
   f.l[0].n_compute = grid - n_comm0;
   f.l[0].stream = 1;
+  f.l[0].pull_local = 1;
   f.l[0].chunk_ready = x->chunk_ready;
   f.l[0].chunk_tokens = ct;
   f.l[0].split_tail = 0;

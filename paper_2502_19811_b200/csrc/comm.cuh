@@ -88,11 +88,16 @@ __device__ __forceinline__ void comm_init(const LayerArgs& p, uint8_t* smem, int
 // suffix [padrow0, padrow0 + nr).  Returns false for tiles without any.
 __device__ __forceinline__ bool remote_rows(const LayerArgs& p, int q, int& padrow0, int& nr) {
   const int4 pr = reinterpret_cast<const int4*>(p.pairs)[q >> 1];
-  if (!((pr.w >> (q & 1)) & 1)) return false;
   const int base = pr.y + kTileRows * (q & 1);
   const int rows = max(0, min(kTileRows, pr.z - kTileRows * (q & 1)));
+  if (p.pull_local) {  // every row of every populated half (local rows included)
+    padrow0 = base;
+    nr = rows;
+    return nr > 0;
+  }
+  if (!((pr.w >> (q & 1)) & 1)) return false;
   const int rel = base - p.pad_off[pr.x];                        // tile start within the expert block
-  const int first = p.stream ? 0 : min(rows, max(0, p.n_local[pr.x] - rel));  // first remote row
+  const int first = min(rows, max(0, p.n_local[pr.x] - rel));      // first remote row
   padrow0 = base + first;
   nr = rows - first;
   return nr > 0;
@@ -159,7 +164,7 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
             while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
             ready_mask |= 1ull << si;
           }
-          if (p.stream && ti / p.chunk_tokens > chunk_ok) {  // chunks land in order
+          if (p.chunk_ready && ti / p.chunk_tokens > chunk_ok) {  // chunks land in order
             const int c = ti / p.chunk_tokens;
             while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.chunk_ready + c), p.epoch)) __nanosleep(128);
             chunk_ok = c;

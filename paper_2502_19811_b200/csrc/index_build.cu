@@ -175,8 +175,16 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   probe(0);
   // -------- phase 1b: bookkeeping over natural token slices: global
   // histogram (routing.py:78-84), transfer matrix (routing.py:106-117) and
-  // the non-hosted tok_pos slots --------
-  {
+  // the non-hosted tok_pos slots.  The hot path (no reference lists) needs
+  // only the tok_pos slots --------
+  if (!(ix.flags & kIndexRefLists)) {
+    const int t_lo = static_cast<int>(static_cast<long long>(M) * blockIdx.x / gridDim.x);
+    const int t_hi = static_cast<int>(static_cast<long long>(M) * (blockIdx.x + 1) / gridDim.x);
+    for (int i = t_lo * K + tid; i < t_hi * K; i += kThreads) {
+      const int e = __ldg(ix.experts + i);
+      if (e < ix.e_lo || e >= ix.e_lo + Er) ix.tok_pos[i] = -1;
+    }
+  } else {
     int* s_tr = reinterpret_cast<int*>(sh_keys);  // W*W <= 4096 ints (host-checked)
     int* s_hist = s_tr + W * W;                   // E <= 1024 ints
     for (int i = tid; i < W * W; i += kThreads) s_tr[i] = 0;

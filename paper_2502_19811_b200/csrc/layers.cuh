@@ -51,7 +51,9 @@ struct LayerArgs {
   // by the dispatch CTAs once its token's upload chunk landed (chunk_ready
   // epoch, written by the copy stream); layer1 counts finished output halves
   // per token chunk (out_cnt) for the download stream to wait on
-  int stream;
+  int stream;                 // (kept for the host-streamed forward's bookkeeping)
+  int pull_local;             // dispatch CTAs also place the local rows (no dispatch_local launch):
+                              // every populated 128-row half is published by the dispatch
   const uint32_t* chunk_ready;
   int chunk_tokens;
   uint32_t* out_cnt;

@@ -379,12 +379,14 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // "sequential" mode (no overlap, the cli's baseline): the first GEMM
         // waits for the WHOLE dispatch, like an all-to-all before GroupGEMM
         for (int q = 0; q < 2 * P; ++q)
-          if ((reinterpret_cast<const int4*>(p.pairs)[q >> 1].w >> (q & 1)) & 1)
+          if (p.pull_local ? reinterpret_cast<const int4*>(p.pairs)[q >> 1].z > kTileRows * (q & 1)
+                           : (reinterpret_cast<const int4*>(p.pairs)[q >> 1].w >> (q & 1)) & 1)
             while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.xg_ready + q), p.epoch)) __nanosleep(64);
         seq_done = true;
       }
       if (lane == 0) {
-        if (w.layer == 0 && ((pr.w >> cta) & 1) && !(p.debug & 1)) {
+        const bool pulled = p.pull_local ? pr.z > kTileRows * static_cast<int>(cta) : ((pr.w >> cta) & 1);
+        if (w.layer == 0 && pulled && !(p.debug & 1)) {
           // this CTA's 128 A rows include rows pulled over NVLink by a dispatch CTA
           const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
           while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) __nanosleep(32);
