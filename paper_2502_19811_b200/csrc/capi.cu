@@ -994,8 +994,13 @@ int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, 
   f.l[0].split_tail = 0;
   f.l[1].raster = 2;
   f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
-  f.l[1].pairs = x->ix.pairs0;  // (row tile, expert) order; folders claimed last (index build)
-  f.l[1].fuse_combine = 1;
+  f.l[1].pairs = x->ix.pairs0;  // (row tile, expert) order
+  // the dispatch CTAs reduce finished token chunks (no layer1 unit waits for
+  // another); COMET_STREAM_FUSE=1: the epilogue fold (folder claimed last)
+  const bool fold = env_int("COMET_STREAM_FUSE", 0) != 0;
+  f.l[0].stream_combine = fold ? 0 : 1;
+  f.l[1].fuse_combine = fold ? 1 : 0;
+  f.l[1].publish_tiles = 1;
   f.l[1].y_local = x->y_stream;
   f.l[1].out_cnt = x->counters + 2 * x->nb1;
   f.l[1].chunk_tokens = ct;

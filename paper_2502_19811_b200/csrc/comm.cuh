@@ -355,5 +355,120 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
   }
 }
 
+// Streamed single-GPU forward (comet_forward_host): after their dispatch the
+// dispatch CTAs reduce the top-k combine chunk by chunk (token chunk c outer,
+// n-block inner) as soon as the layer1 tiles holding the chunk's rows are
+// published, write y, and count each chunk's finished halves for the
+// download stream (out_cnt).  Layer1 units never wait for each other.
+__device__ void stream_combine(const LayerArgs& p, uint8_t* smem) {
+  const int K = p.topk, N = p.n_embed, NB = p.n_blocks, M = p.M;
+  constexpr uint32_t kSeg = kBlockN * 2;
+  const uint32_t slot_bytes = K * kSeg;
+  const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / slot_bytes)) / kReducers * kReducers;
+  comm_init(p, smem, n_slots);
+  CommSmem* cs = comm_smem(smem);
+  const int n_comm = gridDim.x - p.n_compute;  // (p = layer1 args with n_compute of layer0)
+  const int cid = blockIdx.x - p.n_compute;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ct = p.chunk_tokens;
+  const int n_ch = (M + ct - 1) / ct;
+  auto jobs_of = [&](int c) {
+    const int n_tok = min(ct, M - c * ct);
+    return n_tok > cid ? (n_tok - cid + n_comm - 1) / n_comm : 0;
+  };
+  if (warp == 0) {
+    int k = 0;
+    for (int c = 0; c < n_ch; ++c) {
+      const int jobs = jobs_of(c);
+      for (int nb = 0; nb < NB; ++nb) {
+        const int cols = N - nb * static_cast<int>(kBlockN);
+        const int h_hi = cols > static_cast<int>(kBlockN / 2) ? 1 : 0;
+        const uint32_t seg = min(kSeg, static_cast<uint32_t>(cols) * 2u);
+        for (int j0 = 0; j0 < jobs; j0 += kBatch) {
+          const int j = j0 + lane;
+          if (lane < kBatch && j < jobs) {
+            const int t = c * ct + cid + j * n_comm;
+            const int job = k + lane;
+            const int slot = job % n_slots;
+            JobDesc d;
+            uint32_t bytes = 0;
+            int pos[8];
+            for (int s2 = 0; s2 < K; ++s2) {
+              pos[s2] = p.tok_pos[t * K + s2];
+              d.w[s2] = pos[s2] < 0 ? 0.f : (p.combine_w ? p.combine_w[t * K + s2] : 1.f);
+              bytes += pos[s2] >= 0 ? seg : 0u;
+              if (pos[s2] >= 0)  // the row's layer1 tile of this n-block is in memory
+                for (int h = 0; h <= h_hi; ++h) {
+                  const uint32_t* fl = p.tile_done + (static_cast<long long>(pos[s2] >> 7) * NB + nb) * 2 + h;
+                  while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(128);
+                }
+            }
+            ptx::fence_async_global();  // generic-proxy rows -> bulk (async proxy) loads
+            d.dst = p.y_local + static_cast<long long>(t) * N + nb * kBlockN;
+            ptx::mbar_wait(cs->empty + slot, ((job / n_slots) & 1) ^ 1);
+            cs->desc[slot] = d;
+            ptx::mbar_arrive_expect_tx(cs->full + slot, bytes);
+            for (int s2 = 0; s2 < K; ++s2)
+              if (pos[s2] >= 0)
+                ptx::bulk_load(smem + slot * slot_bytes + s2 * kSeg,
+                               p.yrows + static_cast<long long>(pos[s2]) * N + nb * kBlockN, seg, cs->full + slot);
+          }
+          k += min(kBatch, jobs - j0);
+          __syncwarp();
+        }
+      }
+    }
+    return;
+  }
+  const int me = warp - 1;
+  int k = 0;
+  for (int c = 0; c < n_ch; ++c) {
+    const int jobs = jobs_of(c);
+    for (int nb = 0; nb < NB; ++nb) {
+      for (int j = 0; j < jobs; ++j, ++k) {
+        if (k % kReducers != me) continue;
+        const int slot = k % n_slots;
+        ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
+        const JobDesc& d = cs->desc[slot];
+        __nv_bfloat16* dst = d.dst;
+        float w[8];
+        for (int s2 = 0; s2 < K; ++s2) w[s2] = d.w[s2];
+        uint4 o[kBlockN / 256];
+#pragma unroll
+        for (int h = 0; h < static_cast<int>(kBlockN / 256); ++h) {
+          float acc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+          for (int s2 = 0; s2 < K; ++s2) {  // ascending slot = ascending expert (executor.py:102-120)
+            if (w[s2] == 0.f) continue;
+            const uint4 v = *reinterpret_cast<const uint4*>(smem + slot * slot_bytes + s2 * kSeg + h * 512 + lane * 16);
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __bfloat1622float2(hv[q]);
+              acc[2 * q] += f.x * w[s2];
+              acc[2 * q + 1] += f.y * w[s2];
+            }
+          }
+          o[h].x = pack2(acc[0], acc[1]); o[h].y = pack2(acc[2], acc[3]);
+          o[h].z = pack2(acc[4], acc[5]); o[h].w = pack2(acc[6], acc[7]);
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(cs->empty + slot);
+#pragma unroll
+        for (int h = 0; h < static_cast<int>(kBlockN / 256); ++h)
+          if (nb * kBlockN + h * 256 + lane * 8 < N) ptx::st_v4(dst + h * 256 + lane * 8, o[h]);
+      }
+      // this CTA's tokens of chunk c are final for nb -> count them (copy engine reads y)
+      ptx::named_bar_sync(2, kReducers * 32);
+      if (threadIdx.x == 32 && jobs) {
+        __threadfence_system();
+        const int cols = N - nb * static_cast<int>(kBlockN);
+        atomicAdd(p.out_cnt + c, static_cast<uint32_t>(jobs) * (cols > static_cast<int>(kBlockN / 2) ? 2u : 1u));
+      }
+    }
+  }
+}
+
 }  // namespace comm
 }  // namespace comet

@@ -57,6 +57,9 @@ struct LayerArgs {
   const uint32_t* chunk_ready;
   int chunk_tokens;
   uint32_t* out_cnt;
+  int stream_combine;         // layer0 (streamed forward): dispatch CTAs then reduce finished token
+                              // chunks (comm::stream_combine) instead of joining the GEMMs
+  int publish_tiles;          // layer1: publish tile_done epochs even without the fused combine
   const int32_t* pull_token;  // layer0 comm
   const int32_t* pull_src;
   const int32_t* tok_pos;     // [M*topk]

@@ -317,7 +317,8 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
 
   const int P = f.l[f.mode == 1 ? 1 : 0].meta[kMetaPairs];
   // pairs that compute: everything but layer1 combine CTAs (dispatch CTAs join)
-  const int n_pairs = (f.mode == 1 ? f.l[1].n_compute : static_cast<int>(gridDim.x)) >> 1;
+  const int n_pairs =
+      (f.mode == 1 ? f.l[1].n_compute : (f.l[0].stream_combine ? f.l[0].n_compute : static_cast<int>(gridDim.x))) >> 1;
   Sched s0, s1;
   const int total = seq_total(f, P, n_pairs, s0, s1);
   if (f.mode != 0) {
@@ -718,13 +719,14 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         }
       } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
-        if (p.out_cnt) srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
+        if (p.out_cnt && p.fuse_combine)
+          srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
         // pushed rows become visible to the peer through the releasing
         // thread's system-scope fence in nb_contributed (cumulative over the
         // CTA's stores ordered before it by the barrier) -- one fence per CTA
         // instead of one per thread
         ptx::named_bar_sync(1, 128);
-        if (p.out_cnt && threadIdx.x == kEpiThread0 && amount) {
+        if (p.out_cnt && p.fuse_combine && threadIdx.x == kEpiThread0 && amount) {
           // streamed forward: these output rows' halves are final -> count
           // them per token chunk (rows are token-sorted: few runs) for the
           // download stream; one system fence covers the CTA's stores
@@ -744,7 +746,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (threadIdx.x == kEpiThread0 && amount) {
           __threadfence();
           ptx::red_release_gpu_add(p.nb_done + w.nb, amount);
-          if (p.fuse_combine)
+          if (p.fuse_combine || p.publish_tiles)
             for (int h = h_lo; h <= h_hi; ++h)
               ptx::st_release_gpu(p.tile_done + (static_cast<long long>(row0 >> 7) * NB + w.nb) * 2 + h, p.epoch);
           if (p.world > 1)
@@ -787,6 +789,12 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
     __syncthreads();
     comm::comm_release(f.l[0], smem);
     __syncthreads();
+    if (f.l[0].stream_combine) {  // streamed forward: reduce finished token chunks instead
+      LayerArgs pc = f.l[1];
+      pc.n_compute = f.l[0].n_compute;
+      comm::stream_combine(pc, smem);
+      compute = false;
+    }
   }
   if (compute) compute_role(f, smem, &tm_a0, &tm_b0, &tm_a1, &tm_b1);
 

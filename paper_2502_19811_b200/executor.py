@@ -272,9 +272,11 @@ class MoELayer:
             cw = None if combine_w is None else combine_w.float().contiguous()
             xb = x_host if x_host.dtype == torch.bfloat16 else x_host.to(torch.bfloat16)
             k = self.knobs
+            # the dispatch CTAs also reduce the combine (they do not join the
+            # GEMMs here): a small count
             self.ctx.forward_host(xb.contiguous(), ex.contiguous(), cw, out, M, self.weights.w0t, self.weights.w1t,
-                                  self.act, n_comm0=max(2, k.n_comm0 // 2 * 2), group0=k.group0, wave1=k.wave1,
-                                  chunks=max(1, min(64, M // 1024)))
+                                  self.act, n_comm0=int(os.environ.get("COMET_STREAM_NC", 16)), group0=k.group0,
+                                  wave1=k.wave1, chunks=max(1, min(64, M // 1024)))
             return out
         sizes = _chunk_sizes(M, chunks)
         if world > 1 or len(sizes) <= 1:

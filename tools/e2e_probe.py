@@ -56,10 +56,15 @@ y_dev = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
 layer.place_tokens(x_dev, M)
 t = timed(lambda: layer.run(ex_dev, M, y_dev))
 print(f"device forward: {t:.3f} ms")
-for c in (None, 1, 2, 3, 4, [1024, 3072, 3072, 1024], [2048, 4096, 2048], [1024, 2048, 2048, 2048, 1024],
-          [768, 2304, 2304, 2304, 512], [1536, 2560, 2560, 1536], [1024, 2048, 3072, 1536, 512]):
-    t = timed(lambda: layer.forward_host(x_host, ex_host, out=y_host, chunks=c))
-    print(f"forward_host chunks={c}: {t:.3f} ms")
-for m in (512, 1024, 1536, 2048, 3072, 4096):
+import os
+for rep in range(2):
+    for c in (None, 2, 3):
+        t = timed(lambda: layer.forward_host(x_host, ex_host, out=y_host, chunks=c))
+        print(f"forward_host chunks={c}: {t:.3f} ms")
+    for ch in (8, 16, 32):
+        t = timed(lambda: layer.ctx.forward_host(x_host, ex_host, None, y_host, M, layer.weights.w0t, layer.weights.w1t,
+                                                 0, n_comm0=32, group0=8, wave1=4, chunks=ch))
+        print(f"streamed chunks={ch}: {t:.3f} ms")
+for m in ():
     t = timed(lambda: layer.run(ex_dev[:m], m, y_dev[:m]))
     print(f"device forward M={m}: {t:.3f} ms")
