@@ -120,7 +120,8 @@ class ClockSampler:
 def dist_setup(gpus: int):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    from paper_2502_19811_b200.distributed import local_device
+    local = local_device()  # LOCAL_RANK (COMET_SAME_DEVICE=1: every rank on GPU 0, test mode)
     if world != gpus:
         raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
     import torch
@@ -128,7 +129,11 @@ def dist_setup(gpus: int):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("COMET_DIST_BACKEND", "nccl")  # gloo: ranks sharing one GPU (test mode)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -137,7 +142,8 @@ def max_over_ranks(v: float, world: int) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -19,11 +19,21 @@ import numpy as np
 from .config import ConfigurationError, ModelConfig, ParallelSpec
 
 
+def local_device() -> int:
+    """This process's GPU: LOCAL_RANK, or 0 for every rank when
+    COMET_SAME_DEVICE=1 (all ranks of a group sharing one GPU -- the
+    multi-process IPC path exercised on a single-GPU box, with the layer grid
+    split by COMET_GRID so the ranks' persistent kernels are co-resident)."""
+    if os.environ.get("COMET_SAME_DEVICE", "0") != "0":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", 0))
+
+
 def world_info():
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized():
-        return 0, 1, int(os.environ.get("LOCAL_RANK", 0))
-    return dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", dist.get_rank()))
+        return 0, 1, local_device()
+    return dist.get_rank(), dist.get_world_size(), local_device()
 
 
 def exchange_handles(handle: bytes, group=None) -> bytes:
