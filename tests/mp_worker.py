@@ -34,7 +34,9 @@ def main():
     cw = np.random.default_rng(74).random((M, topk)).astype(np.float32)
     dev = distributed.local_device()
     rw = RankWeights.from_full(w.w0, w.w1, model, par, rank, device=dev)
-    layer = distributed.init_layer(model, par, M, rw, activation="tanh", knobs=LayerKnobs(n_comm0=8))
+    grid = int(os.environ.get("COMET_GRID", 148))
+    layer = distributed.init_layer(model, par, M, rw, activation="tanh",
+                                   knobs=LayerKnobs(n_comm0=min(8, max(2, grid // 2 // 2 * 2))))
     lo, hi = layer.token_range(M)
     ex = torch.from_numpy(routing.as_array().copy()).cuda(dev)
     outs = []
