@@ -295,6 +295,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       {&ix.chunk_cnt, (size_t)x->E_r * kIndexMaxChunks},
       {&ix.chunk_loc, (size_t)x->E_r * kIndexMaxChunks},
       {&ix.pair_key, (size_t)x->cap_pairs},
+      {reinterpret_cast<int32_t**>(&ix.fold_part), (size_t)2 * 160 * std::min(x->E_r, 64)},
   };
   size_t total = 0;
   for (auto& p : parts) total += align_up(p.n * 4, 256);
@@ -901,8 +902,12 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
                   int wave1, void* stream) {
   // hot path: no reference-format tile lists; combine list only for comm-CTA combine
   // (the combine list only feeds world-1 combine CTAs; world > 1 fuses the combine)
+  // world > 1 with fold chains (several hosted experts per token): order the
+  // layer1 pairs by fold level (COMET_FOLD_ORDER=0 keeps expert order)
+  const bool fold_order = x->cfg.world > 1 && x->E_r > 1 && x->E_r <= 64 && x->cfg.topk > 1 &&
+                          env_int("COMET_FOLD_ORDER", 1) != 0;
   const int flags = (x->cfg.world == 1 && n_comm1 > 0 ? kIndexCombineList : 0) |
-                    (x->cfg.world > 1 ? kIndexSignal : 0);
+                    (x->cfg.world > 1 ? kIndexSignal : 0) | (fold_order ? kIndexFoldOrder : 0);
   if (int rc = comet_index_build_ex(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), flags,
                                     stream))
     return rc;

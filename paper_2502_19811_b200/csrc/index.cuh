@@ -31,7 +31,9 @@ enum MetaSlot : int {
 constexpr int kIndexRefLists = 1;      // reference tiles0 / tiles1 / chunks (resolver API)
 constexpr int kIndexCombineList = 2;   // combine token list (comm-CTA combine)
 constexpr int kIndexSignal = 4;        // publish this rank's x_ready epoch to every peer
-constexpr int kIndexStream = 8;        // host-streamed forward: pairs in (row tile, expert) order and,
+constexpr int kIndexStream = 8;        // host-streamed forward: pairs in (row tile, expert) order
+constexpr int kIndexFoldOrder = 16;    // fused combine with fold chains: order pairs1 by fold level
+                                       // (experts whose rows are only folded in come first) and,
                                        // per token, the fused-combine folder = its row claimed LAST
 constexpr int kIndexMaxChunks = 64;    // token chunks per hosted expert (host-checked)
 
@@ -75,6 +77,7 @@ struct IndexDev {
   uint32_t* gbar;       // [2] grid barrier: arrival count (self-resetting), generation
   int32_t* chunk_cnt;   // [E_r * kIndexMaxChunks] hits per (hosted expert, token chunk)
   int32_t* chunk_loc;   // [E_r * kIndexMaxChunks] local-token hits per (hosted expert, chunk)
+  unsigned long long* fold_part;  // [grid * E_r] per-CTA fold-predecessor masks (kIndexFoldOrder)
   uint32_t* zero_words; // layer1 per-n-block counters, zeroed every build
   int n_zero_words;
 

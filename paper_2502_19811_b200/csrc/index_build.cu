@@ -212,6 +212,32 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       if (s_hist[i]) atomicAdd(ix.counts + i, s_hist[i]);
   }
 
+  // fold-predecessor masks of this CTA's token slice: for a token with >= 2
+  // hosted experts, the last hosted one (its fused-combine folder) must come
+  // after every other hosted one in the layer1 order
+  if (ix.flags & kIndexFoldOrder) {
+    unsigned long long* s_pred = reinterpret_cast<unsigned long long*>(sh_keys);  // E_r <= 64 masks
+    __syncthreads();
+    for (int j = tid; j < Er; j += kThreads) s_pred[j] = 0ull;
+    __syncthreads();
+    const int t_lo = static_cast<int>(static_cast<long long>(M) * blockIdx.x / gridDim.x);
+    const int t_hi = static_cast<int>(static_cast<long long>(M) * (blockIdx.x + 1) / gridDim.x);
+    for (int t = t_lo + tid; t < t_hi; t += kThreads) {
+      unsigned long long m = 0ull;
+      int last = -1;
+      for (int sl = 0; sl < K; ++sl) {
+        const int j = __ldg(ix.experts + static_cast<long long>(t) * K + sl) - ix.e_lo;
+        if (j < 0 || j >= Er) continue;
+        if (last >= 0) m |= 1ull << last;
+        last = j;
+      }
+      if (m) atomicOr(s_pred + last, m);
+    }
+    __syncthreads();
+    for (int j = tid; j < Er; j += kThreads) ix.fold_part[static_cast<long long>(blockIdx.x) * Er + j] = s_pred[j];
+    __syncthreads();
+  }
+
   probe(1);
   grid_barrier(ix.gbar, ix.gbar + 1);
   probe(2);
@@ -324,6 +350,40 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     }
     s_t0[Er] = t;
     s_p0[Er] = p;
+  }
+  __syncthreads();
+  // layer1 pair order (pairs1): experts by (fold level, id) -- level = longest
+  // chain of fold predecessors, so a folder's rows come after all the rows it
+  // folds (no fold waits on units running alongside); natural order otherwise
+  __shared__ int s_pord[kMaxExperts];  // first pairs1 index of expert j
+  if (ix.flags & kIndexFoldOrder) {
+    __shared__ unsigned long long s_fp[64];
+    __shared__ int s_lvl[64];
+    for (int j = tid; j < Er; j += kThreads) {
+      unsigned long long m = 0ull;
+      for (int c = 0; c < static_cast<int>(gridDim.x); ++c) m |= __ldcg(ix.fold_part + static_cast<long long>(c) * Er + j);
+      s_fp[j] = m;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int max_lvl = 0;
+      for (int j = 0; j < Er; ++j) {
+        int l = 0;
+        for (int q = 0; q < j; ++q)
+          if ((s_fp[j] >> q) & 1ull) l = max(l, s_lvl[q] + 1);
+        s_lvl[j] = l;
+        max_lvl = max(max_lvl, l);
+      }
+      int off = 0;
+      for (int l = 0; l <= max_lvl; ++l)
+        for (int j = 0; j < Er; ++j)
+          if (s_lvl[j] == l) {
+            s_pord[j] = off;
+            off += s_p0[j + 1] - s_p0[j];
+          }
+    }
+  } else {
+    for (int j = tid; j < Er; j += kThreads) s_pord[j] = s_p0[j];
   }
   __syncthreads();
   const int T0 = s_t0[Er], P = s_p0[Er];
@@ -451,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       int j, prow, valid;
       long long key;
       pair_of(i, j, prow, valid, key);
-      int* o = ix.pairs1 + i * 4;
+      int* o = ix.pairs1 + (s_pord[j] + (i - s_p0[j])) * 4;
       int rank = 0;
       for (int q = 0; q < P; ++q) {
         long long kq;
