@@ -14,8 +14,11 @@ router output, dispatch (local HBM rows + NVLink pulls), fused GroupGEMM FC1
 
 ``value``: tokens already resident in HBM (the symmetric token buffer, where
 the previous layer would have written them).  ``e2e``: the same forward
-through the public per-rank API with HOST (pinned) buffers -- H2D of the
-tokens and the router output and D2H of the result inside the timed region.
+through the public per-rank API with HOST (pinned) buffers -- the tokens and
+the router output cross PCIe to the GPU and the result back inside the timed
+region (one GPU: the zero-copy forward, dispatch CTAs read the tokens from
+pinned host memory and the fused combine writes the output there; multi-GPU:
+copy, forward, copy).
 ``--impl reference`` times the reference algorithm on the host cores (the
 numpy oracle port; the reference package itself is pure Python and cannot
 run a Mixtral layer in bounded time) on a bounded token sample per step,
@@ -390,7 +393,10 @@ def run_ours(args):
             "kernels_ms": ({"layers": round(t_l0, 4)} if fused else {"layer0": round(t_l0, 4), "layer1": round(t_l1, 4)}),
             "unfused_ms": None if unfused_ms is None else round(unfused_ms, 4),
             "speedup_vs_unfused": None if unfused_ms is None else round(unfused_ms / ms, 3),
-            "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": ("MoELayer.forward_host -> comet_forward_zerocopy (pinned host buffers read / written "
+                             "over PCIe by the layer kernel)" if world == 1 and os.environ.get("COMET_E2E", "zerocopy")
+                             == "zerocopy" else "MoELayer.forward_host (H2D, forward, D2H)")},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "knobs": {"n_comm0": knobs.n_comm0, "n_comm1": knobs.n_comm1, "group0": knobs.group0,

@@ -166,6 +166,20 @@ int comet_forward_host(comet_ctx* ctx, const void* h_x, const int32_t* h_experts
                        void* h_y, int M, const void* w0t, const void* w1t, int activation, int n_comm0, int group0,
                        int wave1, int chunks, void* stream);
 
+/* Zero-copy single-GPU forward on pinned HOST buffers (world 1; same
+ * arguments as comet_forward_host without `chunks`).  The host is treated as
+ * the token-owning peer: n_comm0 dispatch CTAs read each token row ONCE from
+ * h_x over PCIe (TMA bulk loads of mapped pinned memory), in the compute
+ * claim order, and fan it out to the token's hosted rows, then join the
+ * GEMMs; layer1's fused combine writes each finished output row straight
+ * into h_y.  Requires topk <= 8 and N % 512 == 0.  Asynchronous on `stream`
+ * (h_y is complete when the stream reaches the end of this call).  Same
+ * arithmetic as execute_naive (executor.py:132-148) within the bf16
+ * tolerance; replaces the reference's host-array call. */
+int comet_forward_zerocopy(comet_ctx* ctx, const void* h_x, const int32_t* h_experts, const float* h_combine_w,
+                           void* h_y, int M, const void* w0t, const void* w1t, int activation, int n_comm0,
+                           int group0, int wave1, void* stream);
+
 /* Device pointers of internal buffers (testing / profiling). */
 void* comet_hidden_buffer(comet_ctx* ctx);   /* H [rows_pad_cap, K/tp] bf16 */
 void* comet_yrows_buffer(comet_ctx* ctx);    /* layer1 rows [rows_pad_cap, N] bf16 */

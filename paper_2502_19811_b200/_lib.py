@@ -32,7 +32,7 @@ EXPORTS = (
     "comet_routing_buffer", "comet_index_build", "comet_index_build_ex", "comet_index_sizes", "comet_index_download",
     "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_layers", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
-    "comet_timeline_enable", "comet_timeline_dump", "comet_router_topk", "comet_forward_host",
+    "comet_timeline_enable", "comet_timeline_dump", "comet_router_topk", "comet_forward_host", "comet_forward_zerocopy",
 )
 ROLES = ("load", "mma", "tmem_wait", "epilogue", "comm")
 
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_timeline_dump": ([vp, vp, c.c_size_t], i32),
         "comet_router_topk": ([vp, i32, i32, i32, i32, i32, vp, vp, vp], i32),
         "comet_forward_host": ([vp, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, i32, vp], i32),
+        "comet_forward_zerocopy": ([vp, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -294,6 +295,15 @@ class Context:
             vp(combine_w_host.data_ptr()) if combine_w_host is not None else None, vp(y_host.data_ptr()), M,
             vp(w0t.data_ptr()), vp(w1t.data_ptr()), activation, n_comm0, group0, wave1, chunks,
             vp(self._stream(stream))))
+
+    def forward_zerocopy(self, x_host, experts_host, combine_w_host, y_host, M: int, w0t, w1t, activation: int = 0,
+                         n_comm0: int = 16, group0: int = 8, wave1: int = 4, stream=None) -> None:
+        """Zero-copy single-GPU forward on pinned host tensors (comet_forward_zerocopy)."""
+        vp = ctypes.c_void_p
+        check(self.lib.comet_forward_zerocopy(
+            self.handle, vp(x_host.data_ptr()), vp(experts_host.data_ptr()),
+            vp(combine_w_host.data_ptr()) if combine_w_host is not None else None, vp(y_host.data_ptr()), M,
+            vp(w0t.data_ptr()), vp(w1t.data_ptr()), activation, n_comm0, group0, wave1, vp(self._stream(stream))))
 
     def timeline_enable(self, cap: int) -> None:
         self._tl_cap = cap

@@ -286,6 +286,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       {&ix.tok_pos, (size_t)c.m_cap * c.topk},
       {&ix.pairs0, (size_t)x->cap_pairs * 4},
       {&ix.pairs1, (size_t)x->cap_pairs * 4},
+      {&ix.claim_of_tile, (size_t)x->cap_rows_pad / kTileRows + 1},
       {&ix.pull_token, (size_t)c.m_cap},
       {&ix.pull_src, (size_t)c.m_cap},
       {&ix.combine_tok, (size_t)c.m_cap},
@@ -732,6 +733,8 @@ static int layer0_args(comet_ctx* x, const void* w0t, int activation, int n_comm
   a.activation = activation;
   a.split_tail = env_int("COMET_SPLIT", 1) != 0;
   a.chunk_rows = std::max(1, std::min(32, env_int("COMET_CHUNK", 32)));
+  a.dedup = 0;
+  a.claim_of_tile = x->ix.claim_of_tile;
   a.pairs = x->ix.pairs0;
   a.out = x->H;
   a.out_ld = x->k_local;
@@ -1024,6 +1027,58 @@ int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, 
   CK(cudaEventRecord(x->ev_down, x->down_stream));
   CK(cudaStreamWaitEvent(st, x->ev_down, 0));  // the caller's stream covers the whole step
   x->last_y = x->y_stream;
+  return COMET_OK;
+}
+
+// Zero-copy single-GPU forward: the host is the source "peer".  The dispatch
+// CTAs read each token row once straight from pinned host memory over PCIe
+// (deduplicated per token, fanned out to its hosted rows) in the compute
+// claim order, then join the GEMMs; layer1's fused combine writes each
+// token's output row straight into pinned host memory.  No staging copies:
+// PCIe traffic is M*N*2 bytes each way, overlapped with the GEMMs.
+int comet_forward_zerocopy(comet_ctx* x, const void* h_x, const int32_t* h_experts, const float* h_combine_w,
+                           void* h_y, int M, const void* w0t, const void* w1t, int activation, int n_comm0, int group0,
+                           int wave1, void* stream) {
+  const auto& c = x->cfg;
+  if (c.world != 1) return fail(COMET_EINVAL, "comet_forward_zerocopy is a single-GPU forward (world=%d)", c.world);
+  if (M < 1 || M > c.m_cap) return fail(COMET_EINVAL, "M=%d outside [1, m_cap=%d]", M, c.m_cap);
+  if (n_comm0 < 2 || (n_comm0 & 1)) return fail(COMET_EINVAL, "zero-copy forward needs n_comm0 >= 2, even");
+  if (c.topk > 8) return fail(COMET_EINVAL, "zero-copy forward fans a token out to <= 8 rows (topk=%d)", c.topk);
+  if (c.N % kBlockN) return fail(COMET_EINVAL, "zero-copy forward needs N %% %d == 0 (N=%d)", kBlockN, c.N);
+  if (!h_x || !h_y || !h_experts) return fail(COMET_EINVAL, "null host buffer");
+  CK(cudaSetDevice(c.device));
+  if (int rc = ensure_work(x)) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaMemcpyAsync(x->routing, h_experts, sizeof(int32_t) * (size_t)M * c.topk, cudaMemcpyHostToDevice, st));
+  const float* cw = nullptr;
+  if (h_combine_w) {
+    if (!x->cw_dev) CK(cudaMalloc(&x->cw_dev, sizeof(float) * (size_t)c.m_cap * c.topk));
+    CK(cudaMemcpyAsync(x->cw_dev, h_combine_w, sizeof(float) * (size_t)M * c.topk, cudaMemcpyHostToDevice, st));
+    cw = x->cw_dev;
+  }
+  // expert-ascending layer1 (fold-level order would put every folder row --
+  // every host write -- into the second half of layer1; expert order spreads
+  // the PCIe writes: 3.49 vs 3.84 ms, tools/stream_probe.py MODE=zc)
+  const bool fold_order = x->E_r > 1 && x->E_r <= 64 && c.topk > 1 && env_int("COMET_FOLD_ORDER", 0) != 0;
+  if (int rc = comet_index_build_ex(x, x->routing, M, 128, c.N >= 512 ? 128 : std::max(1, c.N / 4),
+                                    fold_order ? kIndexFoldOrder : 0, stream))
+    return rc;
+  KernelArgs f{};
+  if (int rc = layer0_args(x, w0t, activation, 0, group0, &f.l[0])) return rc;
+  if (int rc = layer1_args(x, w1t, cw, h_y, 0, wave1, false, &f.l[1])) return rc;
+  f.mode = 2;
+  f.l[0].n_compute = layer_grid(x) - n_comm0;
+  f.l[0].pull_local = 1;
+  f.l[0].dedup = env_int("COMET_ZC_DEDUP", 1) != 0;
+  f.l[0].host_src = static_cast<const __nv_bfloat16*>(h_x);
+  f.l[0].split_tail = env_int("COMET_SPLIT0", 1) != 0;
+  f.l[1].raster = 2;
+  f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
+  f.l[1].fuse_combine = 1;
+  if (x->E_r == 1 || c.topk == 1) f.l[1].pairs = x->ix.pairs0;
+  if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
+  x->last_y = h_y;
+  x->last_combine_w = cw;
   return COMET_OK;
 }
 

@@ -20,6 +20,8 @@ constexpr int kBatch = 16;                 // jobs described per loader pass
 constexpr uint32_t kRingBytes = 192 * 1024;
 constexpr int kFreeLag = 2;                // dispatch: bulk-store groups before a slot is reused
 constexpr int kPubLag = 24;                // dispatch: groups in flight before a tile is published
+constexpr int kJobSlots = 64;              // dedup dispatch ring slots (job descriptions in smem)
+constexpr int kPubBatch = 8;               // dedup dispatch: completed jobs counted per publication pass
 
 struct JobDesc {
   __nv_bfloat16* dst;
@@ -33,6 +35,9 @@ struct CommSmem {
   int pub_tile[64];  // tile | rows << 16 of a pending dispatch chunk
   int pub_rows[64];  // remote rows of that tile
   int pub_job[64];
+  int2 pub_q[64][8];            // dedup dispatch: (claim tile, its pulled-row count) per destination
+  int job_n[kJobSlots];         // dedup dispatch job in a ring slot: destination rows (<= 8)
+  int4 job_dq[kJobSlots][8];    // (padded row, claim tile, tile's pulled-row count) per destination
   unsigned long long pub_t0[64];
   const __nv_bfloat16* xs_peer[kMaxWorld];
 };
@@ -78,7 +83,8 @@ __device__ __forceinline__ void comm_init(const LayerArgs& p, uint8_t* smem, int
     }
     ptx::fence_mbar_init();
   }
-  if (static_cast<int>(threadIdx.x) < p.world) cs->xs_peer[threadIdx.x] = p.xs_peer[threadIdx.x];
+  if (static_cast<int>(threadIdx.x) < p.world)  // zero-copy forward: the tokens come from pinned host memory
+    cs->xs_peer[threadIdx.x] = p.host_src ? p.host_src : p.xs_peer[threadIdx.x];
   __syncthreads();
 }
 
@@ -108,7 +114,7 @@ __device__ __forceinline__ bool remote_rows(const LayerArgs& p, int q, int& padr
 // completed: the storer waited for all groups, the loads were all consumed).
 __device__ __forceinline__ void comm_release(const LayerArgs& p, uint8_t* smem) {
   const uint32_t row_bytes = static_cast<uint32_t>(p.n_embed) * 2u;
-  const int n_slots = min(kMaxSlots, static_cast<int>(kRingBytes / row_bytes));
+  const int n_slots = min(p.dedup ? kJobSlots : kMaxSlots, static_cast<int>(kRingBytes / row_bytes));
   CommSmem* cs = comm_smem(smem);
   for (int i = threadIdx.x; i < n_slots; i += blockDim.x) {
     ptx::mbar_inval(cs->full + i);
@@ -227,6 +233,170 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
         publish_upto(k);
       }
     });
+    ptx::bulk_wait<0>();
+    publish_upto(k);
+  }
+}
+
+// Dedup (a7: one read per (token, rank)): the row of token t that pulls it is
+// its hosted row in the earliest-claimed tile (ties: lower slot); the smem
+// copy is bulk-stored to every hosted row of t.
+__device__ __forceinline__ bool primary_row(const LayerArgs& p, int t, int pos) {
+  const int K = p.topk;
+  const int my_q = p.claim_of_tile[pos >> 7];
+  const int my_s = p.row_widx[pos] - t * K;
+  for (int s2 = 0; s2 < K; ++s2) {
+    if (s2 == my_s) continue;
+    const int pos2 = p.tok_pos[t * K + s2];
+    if (pos2 < 0) continue;
+    const int q2 = p.claim_of_tile[pos2 >> 7];
+    if (q2 < my_q || (q2 == my_q && s2 < my_s)) return false;
+  }
+  return true;
+}
+
+// layer0 dispatch, deduplicated per token (used by the zero-copy single-GPU
+// forward, where every byte crosses PCIe): items in claim order as in
+// dispatch_rows; the loader describes each job (destinations, their claim
+// tiles and tile sizes) in smem, the storer fans the smem copy out and counts
+// landed rows per claim tile in batches.
+__device__ void dispatch_rows_dedup(const LayerArgs& p, uint8_t* smem) {
+  const uint32_t row_bytes = static_cast<uint32_t>(p.n_embed) * 2u;
+  const int n_slots = min(kJobSlots, static_cast<int>(kRingBytes / row_bytes));
+  comm_init(p, smem, n_slots);
+  CommSmem* cs = comm_smem(smem);
+  const int n_comm = gridDim.x - p.n_compute;
+  const int cid = blockIdx.x - p.n_compute;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.topk;
+  if (warp == 0) {
+    uint64_t ready_mask = 1ull << p.rank;
+    int k = 0;
+    for_my_items(p, cid, n_comm, [&](int q, int padrow0, int rb, int re, int nr) {
+      const int n = re - rb;
+      const int pos = padrow0 + rb + lane;
+      const int t = lane < n ? p.gather_row[pos] : 0;
+      const bool prim = lane < n && primary_row(p, t, pos);
+      const unsigned pm = __ballot_sync(0xffffffffu, prim);
+      const int src = src_rank_of(t, p.M, p.world);
+      int nd = 0;
+      int4 dst[8];
+      if (prim)
+        for (int s2 = 0; s2 < K; ++s2) {
+          const int d = p.tok_pos[t * K + s2];
+          if (d >= 0) {
+            const int qd = p.claim_of_tile[d >> 7];
+            int pr0, nrd;
+            remote_rows(p, qd, pr0, nrd);
+            dst[nd++] = make_int4(d, qd, nrd, 0);
+          }
+        }
+      int jj = k;  // job index of this lane's row
+      for (int i = 0; i < lane; ++i) jj += (pm >> i) & 1;
+      for (int i = 0; i < n; ++i) {
+        if (!((pm >> i) & 1)) continue;
+        const int ti = __shfl_sync(0xffffffffu, t, i);
+        const int si = __shfl_sync(0xffffffffu, src, i);
+        if (lane == 0) ptx::mbar_wait(cs->empty + k % n_slots, ((k / n_slots) & 1) ^ 1);
+        __syncwarp();
+        if (lane == i) {  // the slot is free: describe the job for the storer
+          cs->job_n[jj % n_slots] = nd;
+          for (int q2 = 0; q2 < nd; ++q2) cs->job_dq[jj % n_slots][q2] = dst[q2];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (!((ready_mask >> si) & 1)) {
+            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
+            ready_mask |= 1ull << si;
+          }
+          const int slot = k % n_slots;
+          ptx::mbar_arrive_expect_tx(cs->full + slot, row_bytes);  // release: job description visible
+          ptx::bulk_load(smem + slot * row_bytes, cs->xs_peer[si] + static_cast<long long>(ti) * p.n_embed,
+                         row_bytes, cs->full + slot);
+        }
+        ++k;
+      }
+      __syncwarp();
+    });
+    if (lane == 0) {  // sentinel: no more jobs (arrival without bytes completes the phase)
+      const int slot = k % n_slots;
+      ptx::mbar_wait(cs->empty + slot, ((k / n_slots) & 1) ^ 1);
+      cs->job_n[slot] = -1;
+      ptx::mbar_arrive(cs->full + slot);
+    }
+  } else if (warp == 1 && lane == 0) {
+    int k = 0, head = 0, tail = 0, n_rec = 0;
+    constexpr int kAcc = 8;
+    int acc_q[kAcc], acc_n[kAcc], acc_nr[kAcc];
+    unsigned long long acc_t0[kAcc];
+    int n_acc = 0;
+    auto flush = [&](unsigned long long t_done) {
+      for (int i = 0; i < n_acc; ++i) {
+        const int qd = acc_q[i], nrd = acc_nr[i];
+        const uint32_t prev = ptx::atom_acq_rel_gpu_add(p.xg_cnt + qd, static_cast<uint32_t>(acc_n[i]));
+        if (prev + static_cast<uint32_t>(acc_n[i]) == static_cast<uint32_t>(nrd)) {
+          p.xg_cnt[qd] = 0u;  // last rows of claim tile qd; ready for the next launch
+          comm_record(p, n_rec++, qd, acc_t0[i], t_done);
+          ptx::st_release_gpu(p.xg_ready + qd, p.epoch);
+        }
+      }
+      n_acc = 0;
+    };
+    auto publish_upto = [&](int done_job) {
+      if (head == tail || cs->pub_job[head & 63] > done_job) return;
+      ptx::fence_async_global();
+      const unsigned long long t_done = ptx::globaltimer();
+      while (head != tail && cs->pub_job[head & 63] <= done_job) {
+        const int e = head & 63;
+        for (int s2 = 0; s2 < cs->pub_tile[e]; ++s2) {
+          const int qd = cs->pub_q[e][s2].x, nrd = cs->pub_q[e][s2].y;
+          int i = 0;
+          while (i < n_acc && acc_q[i] != qd) ++i;
+          if (i == n_acc) {
+            if (n_acc == kAcc) {
+              flush(t_done);
+              i = 0;
+            }
+            acc_q[i] = qd;
+            acc_nr[i] = nrd;
+            acc_n[i] = 0;
+            acc_t0[i] = cs->pub_t0[e];
+            n_acc = i + 1;
+          }
+          ++acc_n[i];
+        }
+        ++head;
+      }
+      flush(t_done);
+    };
+    for (;; ++k) {  // jobs in the loader's order until its sentinel
+      const unsigned long long t_job = ptx::globaltimer();
+      const int slot = k % n_slots;
+      ptx::mbar_wait(cs->full + slot, (k / n_slots) & 1);
+      const int nd = cs->job_n[slot];
+      if (nd < 0) break;
+      const int e = tail & 63;
+      for (int s2 = 0; s2 < nd; ++s2) {
+        const int4 dq = cs->job_dq[slot][s2];
+        ptx::bulk_store(p.xg + static_cast<long long>(dq.x) * p.n_embed, smem + slot * row_bytes, row_bytes);
+        cs->pub_q[e][s2] = make_int2(dq.y, dq.z);
+      }
+      ptx::bulk_commit();
+      ptx::bulk_wait_read<kFreeLag>();
+      if (k >= kFreeLag) ptx::mbar_arrive(cs->empty + (k - kFreeLag) % n_slots);
+      cs->pub_tile[e] = nd;
+      cs->pub_job[e] = k;
+      cs->pub_t0[e] = t_job;
+      ++tail;
+      if (k >= kPubLag && tail - head >= kPubLag + kPubBatch) {
+        ptx::bulk_wait<kPubLag>();
+        publish_upto(k - kPubLag);
+      }
+      if (tail - head >= 60) {
+        ptx::bulk_wait<0>();
+        publish_upto(k);
+      }
+    }
     ptx::bulk_wait<0>();
     publish_upto(k);
   }

@@ -64,6 +64,7 @@ struct IndexDev {
   int32_t* chunks;      // [C*4] (col_start, col_stop, first_tile, n_tiles)
   int32_t* pairs0;      // [P*4] (e_local, pad_row, valid_rows, key) layer0 claim order
   int32_t* pairs1;      // [P*4] (e_local, pad_row, valid_rows, 0) expert/row order
+  int32_t* claim_of_tile;  // [Rpad/128] claim-order tile index (2 * pairs0 rank + half) of a padded tile
   int32_t* pull_token;  // [<=M] remote tokens in first-demand order
   int32_t* pull_src;    // [<=M]
   int32_t* combine_tok; // [<=M] tokens with a hosted expert, ascending (combine CTAs)

@@ -524,6 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
         rank += kq < key;
       }
       ix.pair_key[i] = rank;
+      ix.claim_of_tile[prow >> 7] = 2 * rank;
+      if (valid > kTileRows) ix.claim_of_tile[(prow >> 7) + 1] = 2 * rank + 1;
       // .w: bit h set when 128-row half h holds rows pulled from other ranks
       const int r0 = prow - s_pad[j];
       // streamed forward: every row is pulled by the dispatch CTAs (gated on

@@ -47,6 +47,9 @@ struct LayerArgs {
   uint32_t* xg_ready;         // [Rpad_cap / 128] epoch when a 128-row tile of xg is filled
   uint32_t* xg_cnt;           // [Rpad_cap / 128] remote rows landed per tile (reset by its publisher)
   int chunk_rows;             // layer0 dispatch work item: rows of one tile (1..32)
+  int dedup;                  // dispatch pulls each token once and fans it out (dispatch_rows_dedup)
+  const int32_t* claim_of_tile;   // [Rpad/128] padded tile -> claim-order tile index
+  const __nv_bfloat16* host_src;  // zero-copy forward: token rows read from pinned host memory
   // host-streamed forward (comet_forward_host, world 1): every row is pulled
   // by the dispatch CTAs once its token's upload chunk landed (chunk_ready
   // epoch, written by the copy stream); layer1 counts finished output halves

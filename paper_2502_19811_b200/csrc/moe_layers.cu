@@ -785,7 +785,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
   } else if (f.mode != 1 && b >= f.l[0].n_compute) {
     // layer0 dispatch CTA: pull the remote rows, then join the compute pairs
     ptx::pdl_wait();
-    if (!(f.l[0].debug & 1)) comm::dispatch_rows(f.l[0], smem);
+    if (!(f.l[0].debug & 1)) {
+      if (f.l[0].dedup) comm::dispatch_rows_dedup(f.l[0], smem);
+      else comm::dispatch_rows(f.l[0], smem);
+    }
     __syncthreads();
     comm::comm_release(f.l[0], smem);
     __syncthreads();

@@ -244,7 +244,13 @@ class MoELayer:
         (allocated pinned when None); asynchronous on the current stream like
         ``forward`` (synchronise it before reading ``out``).
 
-        Single GPU, COMET_STREAM=1: ONE streamed launch
+        Single GPU, default (COMET_E2E=zerocopy; pinned ``x_host``/``out``):
+        ONE launch with the host as the token-owning peer
+        (``comet_forward_zerocopy``): dispatch CTAs read each token row once
+        from pinned host memory over PCIe in the compute claim order and the
+        fused combine writes output rows straight to ``out``.
+
+        Single GPU, COMET_E2E=stream: ONE streamed launch
         (``comet_forward_host``): the token upload runs in 1024-token chunks
         whose landing the dispatch CTAs wait for, and the download of each
         chunk starts as soon as the fused combine finished its rows.  Correct
@@ -255,8 +261,9 @@ class MoELayer:
         consecutive forwards over token chunks with the H2D of chunk c+1 and
         the D2H of chunk c-1 on two copy streams under the forward of chunk
         c.  Only the first chunk's upload and the last chunk's download stay
-        exposed (default 3 equal chunks for M >= 6144; ``chunks`` = an int for
-        equal chunks or a list of sizes).  Multi-GPU ranks copy, run, copy."""
+        exposed (COMET_E2E=chunks or an explicit ``chunks``; default 3 equal
+        chunks for M >= 6144; ``chunks`` = an int for equal chunks or a list
+        of sizes).  Multi-GPU ranks copy, run, copy."""
         torch = self.torch
         M = int(experts_host.shape[0])
         N = self.model.N
@@ -265,7 +272,20 @@ class MoELayer:
             out = torch.empty(hi_r - lo_r, N, dtype=torch.bfloat16, pin_memory=True)
         world = self.parallel.world_size
         import os
-        if (world == 1 and chunks is None and os.environ.get("COMET_STREAM", "0") != "0"
+        e2e_mode = os.environ.get("COMET_E2E", "zerocopy")
+        if (world == 1 and chunks is None and e2e_mode == "zerocopy" and self.n_pad == N
+                and N % 512 == 0 and self.model.topk <= 8 and x_host.is_pinned() and out.is_pinned()
+                and out.is_contiguous()):
+            # one launch, the host as the token-owning peer (comet_forward_zerocopy)
+            ex = experts_host if experts_host.dtype == torch.int32 else experts_host.to(torch.int32)
+            cw = None if combine_w is None else combine_w.float().contiguous()
+            xb = x_host if x_host.dtype == torch.bfloat16 else x_host.to(torch.bfloat16)
+            k = self.knobs
+            self.ctx.forward_zerocopy(xb.contiguous(), ex.contiguous(), cw, out, M, self.weights.w0t,
+                                      self.weights.w1t, self.act, n_comm0=int(os.environ.get("COMET_ZC_NC", 16)),
+                                      group0=k.group0, wave1=k.wave1)
+            return out
+        if (world == 1 and chunks is None and e2e_mode == "stream"
                 and self.n_pad == N and x_host.is_pinned() and out.is_pinned() and out.is_contiguous()):
             # one launch streaming the upload / download (comet_forward_host)
             ex = experts_host if experts_host.dtype == torch.int32 else experts_host.to(torch.int32)

@@ -270,7 +270,7 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     par = ParallelSpec()
     routing = build_routing(model, par, WorkloadSpec(M=M, seed=61, std=0.032))
     w = random_weights(model, seed=62)
-    monkeypatch.setenv("COMET_STREAM", "1")
+    monkeypatch.setenv("COMET_E2E", "stream")
     layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0),
                      activation="silu", knobs=LayerKnobs(n_comm0=16))
     x = torch.from_numpy(np.random.default_rng(63).standard_normal((M, N)).astype(np.float32)).to(torch.bfloat16)
@@ -286,4 +286,37 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
     ref = oracle_bf16_inputs(x.float().numpy(), w.w0, w.w1, routing.as_array(), silu, cw.numpy())
     assert_close(outs[0].float().numpy(), ref, what=f"streamed E={E} topk={topk} M={M}")
+    layer.close()
+
+
+@pytest.mark.parametrize("E,topk,M,N,K,dedup", [(8, 2, 5000, 512, 1024, "1"), (8, 2, 5000, 512, 1024, "0"),
+                                                (8, 3, 3000, 1024, 2048, "1"), (16, 4, 700, 512, 512, "1"),
+                                                (8, 2, 100, 512, 2048, "1"), (8, 1, 1000, 512, 1024, "1")])
+def test_zerocopy_host_forward(E, topk, M, N, K, dedup, monkeypatch):
+    """comet_forward_zerocopy: dispatch CTAs read token rows from pinned host
+    memory (once per token with dedup, fanned out to every hosted row), the
+    fused combine writes output rows straight to pinned host memory.
+    Matches the oracle; run-to-run bitwise deterministic; equal to the
+    device-resident forward."""
+    import torch
+    model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
+    par = ParallelSpec()
+    routing = build_routing(model, par, WorkloadSpec(M=M, seed=71, std=0.032))
+    w = random_weights(model, seed=72)
+    monkeypatch.setenv("COMET_ZC_DEDUP", dedup)
+    layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0),
+                     activation="silu", knobs=LayerKnobs(n_comm0=16))
+    x = torch.from_numpy(np.random.default_rng(73).standard_normal((M, N)).astype(np.float32)).to(torch.bfloat16)
+    ex = torch.from_numpy(routing.as_array().copy())
+    cw = torch.from_numpy(np.random.default_rng(74).random((M, topk)).astype(np.float32))
+    outs = []
+    for _ in range(2):
+        out = torch.full((M, N), float("nan"), dtype=torch.bfloat16).pin_memory()
+        layer.forward_host(x.pin_memory(), ex.pin_memory(), cw.pin_memory(), out=out)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
+    ref = oracle_bf16_inputs(x.float().numpy(), w.w0, w.w1, routing.as_array(), silu, cw.numpy())
+    assert_close(outs[0].float().numpy(), ref, what=f"zero-copy E={E} topk={topk} M={M} dedup={dedup}")
     layer.close()

@@ -14,6 +14,8 @@
 #include <vector>
 #include <algorithm>
 #include <random>
+#include <string>
+#include <cstring>
 
 #include "../paper_2502_19811_b200/csrc/ptx.cuh"
 
@@ -157,14 +159,24 @@ __global__ void __launch_bounds__(kThreads, 1) copy_tma_st(const uint8_t* __rest
 }
 
 int main(int argc, char** argv) {
+  const bool host_src = argc > 1 && std::string(argv[1]) == "host";
+  const bool host_dst = argc > 1 && std::string(argv[1]) == "hostdst";
   const int rows = 16384;
   const size_t bytes = (size_t)rows * kRowBytes;
   uint8_t *src, *dst;
   int* perm;
-  cudaMalloc(&src, bytes);
-  cudaMalloc(&dst, bytes);
+  if (host_src) {  // zero-copy: pinned host memory read over PCIe by the kernels
+    cudaHostAlloc(&src, bytes, cudaHostAllocMapped);
+    memset(src, 1, bytes);
+  } else {
+    cudaMalloc(&src, bytes);
+    cudaMemset(src, 1, bytes);
+  }
+  if (host_dst)  // zero-copy writes: pinned host destination written over PCIe
+    cudaHostAlloc(&dst, bytes, cudaHostAllocMapped);
+  else
+    cudaMalloc(&dst, bytes);
   cudaMalloc(&perm, rows * 4);
-  cudaMemset(src, 1, bytes);
   std::vector<int> hp(rows);
   for (int i = 0; i < rows; ++i) hp[i] = i;
   std::shuffle(hp.begin(), hp.end(), std::mt19937(1));
@@ -178,29 +190,28 @@ int main(int argc, char** argv) {
   auto run = [&](const char* name, int ctas, auto launch) {
     for (int w = 0; w < 2; ++w) launch();
     cudaEventRecord(a);
-    const int it = 5;
+    const int it = 3;
     for (int i = 0; i < it; ++i) launch();
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     cudaError_t e = cudaGetLastError();
-    printf("%-34s ctas=%3d  %8.1f GB/s total  %7.1f GB/s per CTA %s\n", name, ctas, bytes * it / (ms * 1e-3) / 1e9,
-           bytes * it / (ms * 1e-3) / 1e9 / ctas, e == cudaSuccess ? "" : cudaGetErrorString(e));
+    // verify a few rows arrived
+    std::vector<uint8_t> chk(64);
+    cudaMemcpy(chk.data(), dst, 64, cudaMemcpyDeviceToHost);
+    printf("%-34s ctas=%3d  %8.1f GB/s total  %7.1f GB/s per CTA %s %s\n", name, ctas, bytes * it / (ms * 1e-3) / 1e9,
+           bytes * it / (ms * 1e-3) / 1e9 / ctas, e == cudaSuccess ? "" : cudaGetErrorString(e), chk[0] == 1 ? "ok" : "BAD");
+    cudaMemset(dst, 0, bytes);
   };
-  for (int ctas : {1, 2, 4, 8, 16}) {
-    for (int slots : {12, 20, 26}) {
-      char nm[64];
-      snprintf(nm, 64, "tma ring %d slots, 1 storer lane", slots);
-      run(nm, ctas, [&] { copy_tma<<<ctas, kThreads, smem>>>(src, dst, perm, rows, slots, 1, 1); });
-      snprintf(nm, 64, "tma ring %d slots, 4 storer warps", slots);
-      run(nm, ctas, [&] { copy_tma<<<ctas, kThreads, smem>>>(src, dst, perm, rows, slots, 1, 4); });
-      snprintf(nm, 64, "tma ring %d slots, st.global warps", slots);
-      run(nm, ctas, [&] { copy_tma_st<<<ctas, kThreads, smem>>>(src, dst, perm, rows, slots); });
-    }
-    run("regs unroll 4", ctas, [&] { copy_regs<4><<<ctas, kThreads>>>(src, dst, perm, rows); });
+  printf("source: %s, destination: %s\n", host_src ? "pinned host (zero-copy)" : "device",
+         host_dst ? "pinned host (zero-copy)" : "device");
+  for (int ctas : {8, 16, 32, 64, 132}) {
+    char nm[64];
+    snprintf(nm, 64, "tma ring 24 slots, 1 storer lane");
+    run(nm, ctas, [&] { copy_tma<<<ctas, kThreads, smem>>>(src, dst, perm, rows, 24, 1, 1); });
     run("regs unroll 8", ctas, [&] { copy_regs<8><<<ctas, kThreads>>>(src, dst, perm, rows); });
-    run("regs unroll 16", ctas, [&] { copy_regs<16><<<ctas, kThreads>>>(src, dst, perm, rows); });
+    run("regs unroll 1", ctas, [&] { copy_regs<1><<<ctas, kThreads>>>(src, dst, perm, rows); });
   }
   return 0;
 }

@@ -56,15 +56,17 @@ y_dev = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
 layer.place_tokens(x_dev, M)
 t = timed(lambda: layer.run(ex_dev, M, y_dev))
 print(f"device forward: {t:.3f} ms")
-import os
 for rep in range(2):
-    for c in (None, 2, 3):
-        t = timed(lambda: layer.forward_host(x_host, ex_host, out=y_host, chunks=c))
-        print(f"forward_host chunks={c}: {t:.3f} ms")
-    for ch in (8, 16, 32):
-        t = timed(lambda: layer.ctx.forward_host(x_host, ex_host, None, y_host, M, layer.weights.w0t, layer.weights.w1t,
-                                                 0, n_comm0=32, group0=8, wave1=4, chunks=ch))
-        print(f"streamed chunks={ch}: {t:.3f} ms")
-for m in ():
-    t = timed(lambda: layer.run(ex_dev[:m], m, y_dev[:m]))
-    print(f"device forward M={m}: {t:.3f} ms")
+    t = timed(lambda: layer.forward_host(x_host, ex_host, out=y_host, chunks=3))
+    print(f"forward_host chunk pipeline (3): {t:.3f} ms")
+    for dd in ("1", "0"):
+        os.environ["COMET_ZC_DEDUP"] = dd
+        for nc in (8, 16, 32):
+            t = timed(lambda: layer.ctx.forward_zerocopy(x_host, ex_host, None, y_host, M, layer.weights.w0t,
+                                                         layer.weights.w1t, 0, n_comm0=nc, group0=8, wave1=4))
+            print(f"zero-copy dedup={dd} n_comm0={nc}: {t:.3f} ms")
+    os.environ["COMET_ZC_DEDUP"] = "1"
+ref = y_host.clone()
+layer.forward_host(x_host, ex_host, out=y_host, chunks=3)
+torch.cuda.synchronize()
+print("zero-copy == chunk pipeline:", torch.equal(ref, y_host), (ref.float() - y_host.float()).abs().max().item())

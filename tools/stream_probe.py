@@ -1,4 +1,6 @@
-"""Timeline of the streamed host forward (comet_forward_host), Mixtral EP=1."""
+"""Timeline of the single-GPU host forwards, Mixtral EP=1: MODE=stream
+(comet_forward_host), MODE=zc (comet_forward_zerocopy), MODE=dev (device
+resident comet_forward, for comparison)."""
 import os
 import statistics
 import sys
@@ -21,10 +23,21 @@ layer = MoELayer(model, par, 0, M, rank_weights_random(model, par, 0, torch.devi
 x_host = torch.randn(M, N).to(torch.bfloat16).pin_memory()
 ex_host = torch.from_numpy(routing.as_array().copy()).pin_memory()
 y_host = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
-for chunks in (8, 16):
+mode = os.environ.get("MODE", "stream")
+ex_dev = ex_host.cuda()
+y_dev = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+x_dev = x_host.cuda()
+layer.place_tokens(x_dev, M)
+for chunks in ((8, 16) if mode == "stream" else (0,)):
     def run():
-        layer.ctx.forward_host(x_host, ex_host, None, y_host, M, layer.weights.w0t, layer.weights.w1t, 0,
-                               n_comm0=nc, group0=g0, wave1=4, chunks=chunks)
+        if mode == "stream":
+            layer.ctx.forward_host(x_host, ex_host, None, y_host, M, layer.weights.w0t, layer.weights.w1t, 0,
+                                   n_comm0=nc, group0=g0, wave1=4, chunks=chunks)
+        elif mode == "zc":
+            layer.ctx.forward_zerocopy(x_host, ex_host, None, y_host, M, layer.weights.w0t, layer.weights.w1t, 0,
+                                       n_comm0=nc, group0=g0, wave1=4)
+        else:
+            layer.run(ex_dev, M, y_dev)
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -34,7 +47,7 @@ for chunks in (8, 16):
         run()
     e.record()
     torch.cuda.synchronize()
-    print(f"chunks={chunks}: {s.elapsed_time(e) / 10:.3f} ms per streamed forward")
+    print(f"{mode} chunks={chunks}: {s.elapsed_time(e) / 10:.3f} ms per forward")
 layer.ctx.timeline_enable(1024)
 torch.cuda.synchronize()
 t_host = torch.cuda.Event(enable_timing=True)
@@ -47,13 +60,17 @@ by = {}
 for c, role, task, s_, e_ in recs:
     by.setdefault(role, []).append((task, (s_ - t0) / 1e3, (e_ - t0) / 1e3, c))
 comm = sorted(by.get("comm", []), key=lambda r: r[2])
-print(f"span {max(r[4] for r in recs) / 1e3 - t0 / 1e3:.1f} us; dispatch items {len(comm)}: "
-      f"done at 10% {comm[len(comm) // 10][2]:.0f} 50% {comm[len(comm) // 2][2]:.0f} 100% {comm[-1][2]:.0f} us")
+print(f"span {max(r[4] for r in recs) / 1e3 - t0 / 1e3:.1f} us")
+if comm:
+    print(f"dispatch items {len(comm)}: done at 10% {comm[len(comm) // 10][2]:.0f} 50% {comm[len(comm) // 2][2]:.0f} "
+          f"100% {comm[-1][2]:.0f} us")
 P = int(layer.ctx.index_meta()[3])
 U0 = P * 28
 mma = by["mma"]
 l0 = sorted(e for t, s_, e, c in mma if t < U0)
 l1 = sorted(s_ for t, s_, e, c in mma if t >= U0)
+l0s = sorted(s_ for t, s_, e, c in mma if t < U0)
+print(f"layer0 units: first start {l0s[0]:.0f}, 10% started {l0s[len(l0s) // 10]:.0f}")
 print(f"layer0 units {len(l0)}: 10% done {l0[len(l0) // 10]:.0f} 50% {l0[len(l0) // 2]:.0f} last {l0[-1]:.0f} us")
 print(f"layer1 units {len(l1)}: first start {l1[0]:.0f}, last end {max(e for t, s_, e, c in mma if t >= U0):.0f} us")
 ld = {(c, t): s_ for t, s_, e, c in by["load"]}
