@@ -956,7 +956,7 @@ int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, 
     CK(cudaEventCreateWithFlags(&x->ev_index, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&x->ev_down, cudaEventDisableTiming));
     CK(cudaMalloc(&x->chunk_ready, sizeof(uint32_t) * kMaxStreamChunks));
-    CK(cudaMalloc(&x->y_stream, (size_t)c.m_cap * c.N * 2));
+    if (!x->y_stream) CK(cudaMalloc(&x->y_stream, (size_t)c.m_cap * c.N * 2));
     CK(cudaMemset(x->chunk_ready, 0, sizeof(uint32_t) * kMaxStreamChunks));
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1059,14 +1059,26 @@ int comet_forward_zerocopy(comet_ctx* x, const void* h_x, const int32_t* h_exper
   // expert-ascending layer1 (fold-level order would put every folder row --
   // every host write -- into the second half of layer1; expert order spreads
   // the PCIe writes: 3.49 vs 3.84 ms, tools/stream_probe.py MODE=zc)
-  const bool fold_order = x->E_r > 1 && x->E_r <= 64 && c.topk > 1 && env_int("COMET_FOLD_ORDER", 0) != 0;
+  // COMET_ZC_ORDER=1: pairs in (row tile, expert) order -- a pair's tokens
+  // were mostly pulled for the same row tile of the previous experts, so the
+  // PCIe bytes per tile are uniform instead of front-loaded (experiment)
+  const bool tile_order = env_int("COMET_ZC_ORDER", 0) != 0;
+  const bool fold_order = !tile_order && x->E_r > 1 && x->E_r <= 64 && c.topk > 1 &&
+                          env_int("COMET_FOLD_ORDER", 0) != 0;
   if (int rc = comet_index_build_ex(x, x->routing, M, 128, c.N >= 512 ? 128 : std::max(1, c.N / 4),
-                                    fold_order ? kIndexFoldOrder : 0, stream))
+                                    (fold_order ? kIndexFoldOrder : 0) | (tile_order ? kIndexStream : 0), stream))
     return rc;
+  // n_dl of the dispatch CTAs download the output afterwards (the fused
+  // combine writes a device copy); n_dl = 0: the epilogues write h_y directly
+  const int n_dl = std::min(n_comm0, std::max(0, env_int("COMET_ZC_DL", 8))) & ~1;
+  if (n_dl > 0 && !x->y_stream) CK(cudaMalloc(&x->y_stream, (size_t)c.m_cap * c.N * 2));
   KernelArgs f{};
   if (int rc = layer0_args(x, w0t, activation, 0, group0, &f.l[0])) return rc;
-  if (int rc = layer1_args(x, w1t, cw, h_y, 0, wave1, false, &f.l[1])) return rc;
+  if (int rc = layer1_args(x, w1t, cw, n_dl > 0 ? static_cast<void*>(x->y_stream) : h_y, 0, wave1, false, &f.l[1]))
+    return rc;
   f.mode = 2;
+  f.n_dl = n_dl;
+  f.y_host = static_cast<__nv_bfloat16*>(h_y);
   f.l[0].n_compute = layer_grid(x) - n_comm0;
   f.l[0].pull_local = 1;
   f.l[0].dedup = env_int("COMET_ZC_DEDUP", 1) != 0;
@@ -1075,7 +1087,22 @@ int comet_forward_zerocopy(comet_ctx* x, const void* h_x, const int32_t* h_exper
   f.l[1].raster = 2;
   f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
   f.l[1].fuse_combine = 1;
-  if (x->E_r == 1 || c.topk == 1) f.l[1].pairs = x->ix.pairs0;
+  if (x->E_r == 1 || c.topk == 1 || tile_order) f.l[1].pairs = x->ix.pairs0;
+  // Interleave the layers (COMET_ZC_ILV groups of lag; 0 = layer1 after all
+  // of layer0): the dispatch is PCIe-paced, so layer0 alone leaves the
+  // tensor cores waiting; layer1 groups of finished pairs fill the gaps and
+  // start the host writes early.  Needs one pair order for both layers: at
+  // world 1 the claim order is expert-ascending like pairs1 (no fold-level
+  // order), and no split tails / split-K.
+  f.interleave = fold_order ? 0 : env_int("COMET_ZC_ILV", 3);
+  if (f.interleave > 0) {
+    f.l[1].pairs = x->ix.pairs0;
+    f.l[1].order_group2 = f.l[0].order_group;
+    f.l[0].split_tail = 0;
+    f.l[0].ksplit_max = 0;
+    f.l[1].ksplit_max = 0;
+    f.l[1].split_units = 0;
+  }
   if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
   x->last_y = h_y;
   x->last_combine_w = cw;

@@ -223,6 +223,36 @@ __device__ __forceinline__ int seq_total(const KernelArgs& f, int P, int n_pairs
 
 // Claimed sequence index -> (layer, pair, n-block, half).
 __device__ __forceinline__ Unit unit_at(const KernelArgs& f, int g, int P, const Sched& s0, const Sched& s1) {
+  if (f.interleave > 0) {
+    // Interleaved fused sequence (layer1 pairs in the layer0 pair order, both
+    // in groups of G pairs, no split tails / split-K): layer0 group k, then
+    // layer1 group k - L.  Layer1 work becomes claimable while layer0 still
+    // waits for its input (zero-copy forward: PCIe-paced dispatch), and its
+    // H rows are L groups old when claimed.  A layer1 unit's fold
+    // predecessors (earlier experts' rows) sit in earlier layer1 groups.
+    const int G = f.l[0].order_group, L = f.interleave;
+    const int NB0 = f.l[0].n_blocks, NB1 = f.l[1].n_blocks;
+    const int n_g = (P + G - 1) / G;
+    int layer = 0, u = 0;
+    for (int k = 0; k < n_g + L; ++k) {
+      if (k < n_g) {
+        const int sz = min(G, P - k * G) * NB0;
+        if (g < sz) { layer = 0; u = k * G * NB0 + g; break; }
+        g -= sz;
+      }
+      if (k >= L) {
+        const int j = k - L;
+        const int sz = min(G, P - j * G) * NB1;
+        if (g < sz) { layer = 1; u = j * G * NB1 + g; break; }
+        g -= sz;
+      }
+    }
+    const LayerArgs& p = f.l[layer];
+    Unit w = decode_unit(u, layer, p.raster, P, p.n_blocks, p.order_group, p.order_group2);
+    w.ks = 0;
+    w.half = narrow_block(p, w.nb) ? 0 : -1;
+    return w;
+  }
   int layer = 0;
   Sched s = s0;
   if (g >= s0.total) {
@@ -251,6 +281,52 @@ __device__ __forceinline__ Unit unit_at(const KernelArgs& f, int g, int P, const
 
 __device__ __forceinline__ int slices_of(const Unit& w, const Sched& s0, const Sched& s1) {
   return w.layer ? s1.S : s0.S;
+}
+
+// Zero-copy forward, output side: a downloader CTA walks the layer1 units in
+// sequence order (every n_dl-th), waits for each (128-row tile, 256-column
+// half) to be final (tile_done epoch, published after the fused combine's
+// folder rows were written to the device copy y_local) and copies the folder
+// rows' 512-byte segments to pinned host memory.  Host writes leave the GEMM
+// epilogues (a sysmem store backlog in an SM stalls its epilogue and, through
+// TMEM, its MMAs) and run on these CTAs at PCIe rate.
+__device__ void download_rows(const KernelArgs& f, int did) {
+  const LayerArgs& p = f.l[1];
+  const int NB = p.n_blocks, N = p.n_embed;
+  const int P = p.meta[kMetaPairs];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_warps = blockDim.x >> 5;
+  constexpr int kB = 4;  // row segments in flight per warp
+  for (int u = did; u < P * NB; u += f.n_dl) {
+    const Unit w = decode_unit(u, 1, p.raster, P, NB, p.order_group, p.order_group2);
+    const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
+    for (int cta = 0; cta < 2; ++cta) {
+      const int rows = min(kTileRows, pr.z - kTileRows * cta);
+      if (rows <= 0) continue;
+      const int tile = (pr.y >> 7) + cta;
+      for (int h = 0; h < 2; ++h) {
+        if (lane == 0) {
+          const uint32_t* fl = p.tile_done + (static_cast<long long>(tile) * NB + w.nb) * 2 + h;
+          while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(128);
+        }
+        __syncwarp();
+        const long long col = static_cast<long long>(w.nb) * kBlockN + h * kHalfN + lane * 8;
+        for (int r0 = warp * kB; r0 < rows; r0 += n_warps * kB) {
+          uint4 v[kB];
+          int t[kB];
+#pragma unroll
+          for (int i = 0; i < kB; ++i) {
+            const int rd = r0 + i < rows ? p.row_dst[tile * kTileRows + r0 + i] : -1;
+            t[i] = rd >= 0 ? (rd & 0xFFFFFF) : -1;
+            if (t[i] >= 0) v[i] = __ldcg(reinterpret_cast<const uint4*>(p.y_local + t[i] * static_cast<long long>(N) + col));
+          }
+#pragma unroll
+          for (int i = 0; i < kB; ++i)
+            if (t[i] >= 0) *reinterpret_cast<uint4*>(f.y_host + t[i] * static_cast<long long>(N) + col) = v[i];
+        }
+      }
+    }
+  }
 }
 
 // Compute role of a 2-CTA pair: scheduler (leader warp 3) claims units and
@@ -792,7 +868,10 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
     __syncthreads();
     comm::comm_release(f.l[0], smem);
     __syncthreads();
-    if (f.l[0].stream_combine) {  // streamed forward: reduce finished token chunks instead
+    if (b - f.l[0].n_compute < f.n_dl) {  // zero-copy forward: download the output instead
+      download_rows(f, b - f.l[0].n_compute);
+      compute = false;
+    } else if (f.l[0].stream_combine) {  // streamed forward: reduce finished token chunks instead
       LayerArgs pc = f.l[1];
       pc.n_compute = f.l[0].n_compute;
       comm::stream_combine(pc, smem);

@@ -289,13 +289,20 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     layer.close()
 
 
-@pytest.mark.parametrize("E,topk,M,N,K,dedup", [(8, 2, 5000, 512, 1024, "1"), (8, 2, 5000, 512, 1024, "0"),
-                                                (8, 3, 3000, 1024, 2048, "1"), (16, 4, 700, 512, 512, "1"),
-                                                (8, 2, 100, 512, 2048, "1"), (8, 1, 1000, 512, 1024, "1")])
-def test_zerocopy_host_forward(E, topk, M, N, K, dedup, monkeypatch):
+@pytest.mark.parametrize("E,topk,M,N,K,dedup,ilv,dl", [
+    (8, 2, 5000, 512, 1024, "1", "2", "8"), (8, 2, 5000, 512, 1024, "0", "2", "8"),
+    (8, 2, 5000, 512, 1024, "1", "0", "0"), (8, 2, 5000, 512, 1024, "1", "1", "16"),
+    (8, 3, 3000, 1024, 2048, "1", "2", "8"), (16, 4, 700, 512, 512, "1", "2", "2"),
+    (16, 4, 700, 512, 512, "1", "0", "8"), (8, 2, 100, 512, 2048, "1", "2", "8"),
+    (8, 1, 1000, 512, 1024, "1", "2", "0"), (8, 2, 6000, 1024, 3200, "1", "3", "8"),
+    (8, 2, 300, 512, 2048, "1", "0", "8")])
+def test_zerocopy_host_forward(E, topk, M, N, K, dedup, ilv, dl, monkeypatch):
     """comet_forward_zerocopy: dispatch CTAs read token rows from pinned host
     memory (once per token with dedup, fanned out to every hosted row), the
-    fused combine writes output rows straight to pinned host memory.
+    fused combine writes output rows straight to pinned host memory; layer1
+    groups interleaved with layer0 groups at lag ``ilv`` (0 = after layer0);
+    ``dl`` dispatch CTAs download the output afterwards (0: epilogues write
+    the host rows; M=300 runs layer1 split-K).
     Matches the oracle; run-to-run bitwise deterministic; equal to the
     device-resident forward."""
     import torch
@@ -304,6 +311,8 @@ def test_zerocopy_host_forward(E, topk, M, N, K, dedup, monkeypatch):
     routing = build_routing(model, par, WorkloadSpec(M=M, seed=71, std=0.032))
     w = random_weights(model, seed=72)
     monkeypatch.setenv("COMET_ZC_DEDUP", dedup)
+    monkeypatch.setenv("COMET_ZC_ILV", ilv)
+    monkeypatch.setenv("COMET_ZC_DL", dl)
     layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0),
                      activation="silu", knobs=LayerKnobs(n_comm0=16))
     x = torch.from_numpy(np.random.default_rng(73).standard_normal((M, N)).astype(np.float32)).to(torch.bfloat16)
@@ -318,5 +327,5 @@ def test_zerocopy_host_forward(E, topk, M, N, K, dedup, monkeypatch):
     assert torch.equal(outs[0], outs[1])
     silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
     ref = oracle_bf16_inputs(x.float().numpy(), w.w0, w.w1, routing.as_array(), silu, cw.numpy())
-    assert_close(outs[0].float().numpy(), ref, what=f"zero-copy E={E} topk={topk} M={M} dedup={dedup}")
+    assert_close(outs[0].float().numpy(), ref, what=f"zero-copy E={E} topk={topk} M={M} dedup={dedup} ilv={ilv} dl={dl}")
     layer.close()

@@ -54,8 +54,11 @@ t_host = torch.cuda.Event(enable_timing=True)
 run()
 torch.cuda.synchronize()
 recs = layer.ctx.timeline_dump()
+life = [r for r in recs if r[1] == "tmem_wait" and r[2] == (1 << 20) - 2]
 recs = [r for r in recs if not (r[1] == "tmem_wait" and r[2] == (1 << 20) - 2)]
 t0 = min(r[3] for r in recs)
+if life:
+    print(f"CTA exits: first {(min(r[4] for r in life) - t0) / 1e3:.0f}, last {(max(r[4] for r in life) - t0) / 1e3:.0f} us")
 by = {}
 for c, role, task, s_, e_ in recs:
     by.setdefault(role, []).append((task, (s_ - t0) / 1e3, (e_ - t0) / 1e3, c))
@@ -66,17 +69,39 @@ if comm:
           f"100% {comm[-1][2]:.0f} us")
 P = int(layer.ctx.index_meta()[3])
 U0 = P * 28
+ilv = int(os.environ.get("COMET_ZC_ILV", 3)) if mode == "zc" else 0
+
+
+def seq_layer(g):
+    """Sequence index -> layer (the interleaved zero-copy sequence, unit_at)."""
+    if ilv <= 0:
+        return 0 if g < U0 else 1
+    n_g = (P + g0 - 1) // g0
+    for k in range(n_g + ilv):
+        if k < n_g:
+            sz = min(g0, P - k * g0) * 28
+            if g < sz:
+                return 0
+            g -= sz
+        if k >= ilv:
+            sz = min(g0, P - (k - ilv) * g0) * 8
+            if g < sz:
+                return 1
+            g -= sz
+    return 1
+
+
 mma = by["mma"]
-l0 = sorted(e for t, s_, e, c in mma if t < U0)
-l1 = sorted(s_ for t, s_, e, c in mma if t >= U0)
-l0s = sorted(s_ for t, s_, e, c in mma if t < U0)
+l0 = sorted(e for t, s_, e, c in mma if seq_layer(t) == 0)
+l1 = sorted(s_ for t, s_, e, c in mma if seq_layer(t) == 1)
+l0s = sorted(s_ for t, s_, e, c in mma if seq_layer(t) == 0)
 print(f"layer0 units: first start {l0s[0]:.0f}, 10% started {l0s[len(l0s) // 10]:.0f}")
 print(f"layer0 units {len(l0)}: 10% done {l0[len(l0) // 10]:.0f} 50% {l0[len(l0) // 2]:.0f} last {l0[-1]:.0f} us")
-print(f"layer1 units {len(l1)}: first start {l1[0]:.0f}, last end {max(e for t, s_, e, c in mma if t >= U0):.0f} us")
+print(f"layer1 units {len(l1)}: first start {l1[0]:.0f}, last end {max(e for t, s_, e, c in mma if seq_layer(t) == 1):.0f} us")
 ld = {(c, t): s_ for t, s_, e, c in by["load"]}
-d0 = [e - max(s_, ld.get((c, t), s_)) for t, s_, e, c in mma if t < U0]
-d1 = [e - max(s_, ld.get((c, t), s_)) for t, s_, e, c in mma if t >= U0]
+d0 = [e - max(s_, ld.get((c, t), s_)) for t, s_, e, c in mma if seq_layer(t) == 0]
+d1 = [e - max(s_, ld.get((c, t), s_)) for t, s_, e, c in mma if seq_layer(t) == 1]
 print(f"MMA compute per unit: L0 {statistics.mean(d0):.1f} us, L1 {statistics.mean(d1):.1f} us")
 ep = by["epilogue"]
-print(f"epilogue: L0 {statistics.mean(e - s_ for t, s_, e, c in ep if t < U0):.1f} us, "
-      f"L1 {statistics.mean(e - s_ for t, s_, e, c in ep if t >= U0):.1f} us (max {max(e - s_ for t, s_, e, c in ep if t >= U0):.1f})")
+print(f"epilogue: L0 {statistics.mean(e - s_ for t, s_, e, c in ep if seq_layer(t) == 0):.1f} us, "
+      f"L1 {statistics.mean(e - s_ for t, s_, e, c in ep if seq_layer(t) == 1):.1f} us (max {max(e - s_ for t, s_, e, c in ep if seq_layer(t) == 1):.1f})")
