@@ -164,6 +164,20 @@ def test_mixtral_full_size_vs_torch_fp32_and_determinism():
     assert torch.equal(y1, y2)  # run-to-run bitwise deterministic (ordered combine)
     ref = torch_reference(x, w0, w1, ex.long(), combine_w=cw)
     assert_close(y1.float().cpu().numpy(), ref.cpu().numpy(), what="Mixtral M=8192 EP=1")
+    # size-independent property at full size: permuting the tokens permutes
+    # the output rows bitwise (a row's products accumulate in a fixed order
+    # wherever its tile lands; the combine order is per token)
+    perm = torch.randperm(8192, generator=torch.Generator().manual_seed(5)).cuda()
+    yp = layer.forward(x[perm], ex[perm].contiguous(), cw[perm].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(yp, y1[perm])
+    # the zero-copy host forward (tokens read / output written over PCIe by
+    # the layer kernel) at full size: same tolerance, run-to-run bitwise
+    x_h, ex_h, cw_h = x.to(torch.bfloat16).cpu().pin_memory(), ex.cpu().pin_memory(), cw.cpu().pin_memory()
+    yh = [layer.forward_host(x_h, ex_h, cw_h) for _ in range(2)]
+    torch.cuda.synchronize()
+    assert torch.equal(yh[0], yh[1])
+    assert_close(yh[0].float().numpy(), ref.cpu().numpy(), what="Mixtral M=8192 EP=1 zero-copy host forward")
     layer.close()
 
 
