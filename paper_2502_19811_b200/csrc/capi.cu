@@ -850,6 +850,9 @@ int comet_layers(comet_ctx* x, const void* w0t, const void* w1t, const float* co
   // world > 1: the dispatch CTAs place the local rows too (locality-first:
   // they are the first tiles claimed), saving the local-dispatch launch
   f.l[0].pull_local = x->cfg.world > 1 && env_int("COMET_PULL_LOCAL", 1) != 0;
+  // per-token dedup of the NVLink pulls (dispatch_rows_dedup; one read per
+  // (token, rank), fanned out to the token's hosted rows)
+  f.l[0].dedup = f.l[0].pull_local && x->cfg.topk <= 8 && env_int("COMET_DEDUP", 0) != 0;
   if (!f.l[0].pull_local)
     if (int rc = dispatch_local(x, st)) return rc;
   if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
