@@ -167,12 +167,12 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
         const int si = __shfl_sync(0xffffffffu, src, i);
         if (lane == 0) {
           if (!((ready_mask >> si) & 1)) {
-            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
+            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) sp.pause(64, 7); }
             ready_mask |= 1ull << si;
           }
           if (p.chunk_ready && ti / p.chunk_tokens > chunk_ok) {  // chunks land in order
             const int c = ti / p.chunk_tokens;
-            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.chunk_ready + c), p.epoch)) __nanosleep(128);
+            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.chunk_ready + c), p.epoch)) sp.pause(128, 8); }
             chunk_ok = c;
           }
           const int job = k + i;
@@ -306,7 +306,7 @@ __device__ void dispatch_rows_dedup(const LayerArgs& p, uint8_t* smem) {
         __syncwarp();
         if (lane == 0) {
           if (!((ready_mask >> si) & 1)) {
-            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) __nanosleep(64);
+            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) sp.pause(64, 9); }
             ready_mask |= 1ull << si;
           }
           const int slot = k % n_slots;
@@ -425,7 +425,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
     // ---- loader warp ----
     if (p.world > 1) {  // every peer finished its previous forward (epoch barrier)
       if (lane < p.world)
-        while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + lane), p.epoch)) __nanosleep(64);
+        { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + lane), p.epoch)) sp.pause(64, 10); }
       __syncwarp();
     }
     int k = 0;
@@ -433,7 +433,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
       const int nb_cols = p.out_ld - nb * static_cast<int>(kBlockN);  // a ragged last block <= 256 wide
       const uint32_t nb_target = (nb_cols > 0 && nb_cols <= static_cast<int>(kBlockN / 2)) ? target / 2 : target;
       if (lane == 0)
-        while (ptx::ld_acquire_gpu(p.nb_done + nb) < nb_target) __nanosleep(128);
+        { ptx::Spin sp; while (ptx::ld_acquire_gpu(p.nb_done + nb) < nb_target) sp.pause(128, 11); }
       __syncwarp();
       const unsigned long long t_nb = ptx::globaltimer();
       const uint32_t seg = min(kSeg, static_cast<uint32_t>(N - nb * kBlockN) * 2u);
@@ -570,7 +570,7 @@ __device__ void stream_combine(const LayerArgs& p, uint8_t* smem) {
               if (pos[s2] >= 0)  // the row's layer1 tile of this n-block is in memory
                 for (int h = 0; h <= h_hi; ++h) {
                   const uint32_t* fl = p.tile_done + (static_cast<long long>(pos[s2] >> 7) * NB + nb) * 2 + h;
-                  while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(128);
+                  { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) sp.pause(128, 12); }
                 }
             }
             ptx::fence_async_global();  // generic-proxy rows -> bulk (async proxy) loads

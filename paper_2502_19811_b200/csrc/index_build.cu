@@ -117,7 +117,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen) {
       __threadfence();
       atomicAdd(gen, 1u);
     } else {
-      while (*reinterpret_cast<volatile uint32_t*>(gen) == g) __nanosleep(32);
+      { ptx::Spin sp; while (*reinterpret_cast<volatile uint32_t*>(gen) == g) sp.pause(32, 13); }
     }
     __threadfence();
   }

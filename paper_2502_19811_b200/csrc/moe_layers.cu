@@ -307,7 +307,7 @@ __device__ void download_rows(const KernelArgs& f, int did) {
       for (int h = 0; h < 2; ++h) {
         if (lane == 0) {
           const uint32_t* fl = p.tile_done + (static_cast<long long>(tile) * NB + w.nb) * 2 + h;
-          while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(128);
+          { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) sp.pause(128, 1); }
         }
         __syncwarp();
         const long long col = static_cast<long long>(w.nb) * kBlockN + h * kHalfN + lane * 8;
@@ -458,7 +458,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         for (int q = 0; q < 2 * P; ++q)
           if (p.pull_local ? reinterpret_cast<const int4*>(p.pairs)[q >> 1].z > kTileRows * (q & 1)
                            : (reinterpret_cast<const int4*>(p.pairs)[q >> 1].w >> (q & 1)) & 1)
-            while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.xg_ready + q), p.epoch)) __nanosleep(64);
+            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.xg_ready + q), p.epoch)) sp.pause(64, 2); }
         seq_done = true;
       }
       if (lane == 0) {
@@ -466,13 +466,13 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (w.layer == 0 && pulled && !(p.debug & 1)) {
           // this CTA's 128 A rows include rows pulled over NVLink by a dispatch CTA
           const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
-          while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) __nanosleep(32);
+          { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) sp.pause(32, 3); }
           ptx::fence_async_global();
         } else if (w.layer == 1 && f.mode == 2) {
           // layer1 A = H rows written by the layer0 epilogues of this launch
           const uint32_t* hc = f.h_cnt + (row0 >> 7);
           const uint32_t target = tile_halves(f.l[0]);
-          while (ptx::ld_acquire_gpu(hc) < target) __nanosleep(32);
+          { ptx::Spin sp; while (ptx::ld_acquire_gpu(hc) < target) sp.pause(32, 4); }
           ptx::fence_async_global();
         }
       }
@@ -622,7 +622,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           if (pos < 0) continue;
           for (int h = h_lo; h <= h_hi; ++h) {
             const uint32_t* fl = p.tile_done + (static_cast<long long>(pos >> 7) * NB + w.nb) * 2 + h;
-            while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) __nanosleep(64);
+            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) sp.pause(64, 5); }
           }
         }
       };
@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(256) combine_finish_kernel(const LayerArgs p, 
   const int start = token_start_of(p.rank, p.M, W);
   const int n_own = token_stop_of(p.rank, p.M, W) - start;
   for (int i = threadIdx.x; i < W * NB; i += blockDim.x)
-    while (!ptx::epoch_reached(ptx::ld_acquire_sys(cb_flag + i), p.epoch)) __nanosleep(64);
+    { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(cb_flag + i), p.epoch)) sp.pause(64, 6); }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int vec = N / 8;

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 namespace comet {
@@ -369,6 +370,32 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
+
+// Bounded spin for cross-CTA / cross-rank flag waits: sleeps `ns` per poll
+// and, if one wait exceeds kSpinTimeoutNs (a peer that never signals: a bug
+// or a dead rank), prints the site and traps so the launch fails loudly
+// instead of hanging the GPU.  The clock is read every 64 polls; the report
+// is out of line (no stack or registers in the callers' hot code).
+constexpr unsigned long long kSpinTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__device__ __noinline__ inline void spin_timeout(int site) {
+  printf("comet: device wait timed out (site %d, block %d, thread %d)\n", site, static_cast<int>(blockIdx.x),
+         static_cast<int>(threadIdx.x));
+  __trap();
+}
+struct Spin {
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+  __device__ __forceinline__ void pause(unsigned ns, int site) {
+    __nanosleep(ns);
+    if ((++n & 63u) != 0u) return;
+    const unsigned long long t = globaltimer();
+    if (t0 == 0) {
+      t0 = t;
+    } else if (t - t0 > kSpinTimeoutNs) {
+      spin_timeout(site);
+    }
+  }
+};
 
 }  // namespace ptx
 }  // namespace comet
