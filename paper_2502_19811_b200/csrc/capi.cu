@@ -31,6 +31,8 @@ __global__ void dispatch_local_kernel(const int32_t* gather_row, const int32_t* 
 __global__ void combine_local_kernel(const int32_t* tok_pos, const float* combine_w, const __nv_bfloat16* yrows,
                                      __nv_bfloat16* y, int t0, int n_tok, int topk, int n_embed);
 }  // namespace comet
+cudaError_t set_spin_timeout_index(unsigned long long ns);
+cudaError_t set_spin_timeout_layers(unsigned long long ns);
 
 using namespace comet;
 
@@ -254,6 +256,11 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
   comet_ctx* x = new comet_ctx();
   x->cfg = c;
   CK(cudaSetDevice(c.device));
+  {  // device-wait timeout of the flag spins (ptx::Spin), COMET_SPIN_TIMEOUT_MS
+    const unsigned long long ms = static_cast<unsigned long long>(std::max(1, env_int("COMET_SPIN_TIMEOUT_MS", 30000)));
+    CK(set_spin_timeout_index(ms * 1000000ull));
+    CK(set_spin_timeout_layers(ms * 1000000ull));
+  }
   int32_t info[4];
   if (int rc = comet_device_info(c.device, info)) { delete x; return rc; }
   x->n_sm = info[0];

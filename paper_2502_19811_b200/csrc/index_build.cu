@@ -613,3 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
 }
 
 }  // namespace comet
+
+// host: this unit's device-wait timeout (ptx::Spin)
+cudaError_t set_spin_timeout_index(unsigned long long ns) {
+  return cudaMemcpyToSymbol(comet::ptx::g_spin_timeout_ns, &ns, sizeof(ns));
+}

@@ -1053,3 +1053,8 @@ __global__ void signal_x_ready_kernel(uint32_t* const* x_ready_peer, int rank, i
 }
 
 }  // namespace comet
+
+// host: this unit's device-wait timeout (ptx::Spin)
+cudaError_t set_spin_timeout_layers(unsigned long long ns) {
+  return cudaMemcpyToSymbol(comet::ptx::g_spin_timeout_ns, &ns, sizeof(ns));
+}

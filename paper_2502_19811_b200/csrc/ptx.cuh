@@ -372,11 +372,13 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
 }
 
 // Bounded spin for cross-CTA / cross-rank flag waits: sleeps `ns` per poll
-// and, if one wait exceeds kSpinTimeoutNs (a peer that never signals: a bug
+// and, if one wait exceeds the timeout (a peer that never signals: a bug
 // or a dead rank), prints the site and traps so the launch fails loudly
 // instead of hanging the GPU.  The clock is read every 64 polls; the report
 // is out of line (no stack or registers in the callers' hot code).
-constexpr unsigned long long kSpinTimeoutNs = 30ull * 1000 * 1000 * 1000;
+// per translation unit (no relocatable device code); set at context creation
+// from COMET_SPIN_TIMEOUT_MS by each unit's set_spin_timeout_* (default 30 s)
+static __device__ unsigned long long g_spin_timeout_ns = 30ull * 1000 * 1000 * 1000;
 __device__ __noinline__ inline void spin_timeout(int site) {
   printf("comet: device wait timed out (site %d, block %d, thread %d)\n", site, static_cast<int>(blockIdx.x),
          static_cast<int>(threadIdx.x));
@@ -391,7 +393,7 @@ struct Spin {
     const unsigned long long t = globaltimer();
     if (t0 == 0) {
       t0 = t;
-    } else if (t - t0 > kSpinTimeoutNs) {
+    } else if (t - t0 > g_spin_timeout_ns) {
       spin_timeout(site);
     }
   }
