@@ -548,3 +548,53 @@ def execute_tp_sharded(x, weights: ExpertWeights, routing: RoutingTable, tp: int
         raise ConfigurationError(f"K={routing.model.K} is not divisible by tp={tp}")
     par = ParallelSpec(tp=tp, ep=routing.parallel.ep)
     return _to_numpy(run_emulated(x, weights, routing, par, activation, combine_weights))
+
+
+_RANK_LAYERS: Dict[tuple, "MoELayer"] = {}
+
+
+def execute_scheduled_rank(x_local, w_local: RankWeights, routing: RoutingTable, sched0: Optional[TileSchedule] = None,
+                           sched1: Optional[TileSchedule] = None, activation: Activation = None,
+                           combine_weights=None, layer: Optional["MoELayer"] = None, knobs: Optional[LayerKnobs] = None):
+    """Per-rank form of ``execute_scheduled`` (ref executor.py:
+    180-218) for one process per GPU: this rank's tokens ``x_local``
+    [M_r, N] (the rows ``routing.parallel``'s contiguous pre-distribution
+    gives it, routing.py:86-104) in, this rank's output rows [M_r, N] out, as
+    a bf16 tensor on this rank's GPU.  ``sched0`` / ``sched1`` are this
+    rank's schedules (optional), validated like the reference's.  The first
+    call creates the rank's ``MoELayer`` with ``distributed.init_layer``
+    (collective: every rank calls it, same routing shape) and caches it;
+    ``layer`` passes an existing one.  ``combine_weights`` are the global
+    [M, topk] weights (a rank's combine reads any token's)."""
+    from . import distributed
+    par = routing.parallel
+    rank, world, _ = distributed.world_info()
+    distributed.check_world(par, world)
+    for sched, lay in ((sched0, 0), (sched1, 1)):
+        if sched is None:
+            continue
+        if sched.rank != rank or sched.layer != lay:
+            raise ConfigurationError(f"schedule (rank {sched.rank}, layer {sched.layer}) given to rank {rank} "
+                                     f"as its layer{lay} schedule")
+        bad = validate_schedule(sched, routing, rank)
+        if bad:
+            raise ConfigurationError(f"schedule for rank {rank} is invalid: {bad[0].message}")
+    M = routing.workload.M
+    if layer is not None and layer.act != activation_code(activation):
+        raise ConfigurationError("activation differs from the one the given layer was built with")
+    if layer is None:
+        key = (routing.model, par, M, id(w_local), activation_code(activation))
+        layer = _RANK_LAYERS.get(key)
+        if layer is None:
+            layer = distributed.init_layer(routing.model, par, M, w_local, activation=activation, knobs=knobs)
+            _RANK_LAYERS[key] = layer
+    torch = layer.torch
+    ex = torch.from_numpy(routing.as_array().copy())
+    cw = None if combine_weights is None else torch.as_tensor(np.asarray(combine_weights, np.float32))
+    if not isinstance(x_local, torch.Tensor):
+        x_local = torch.from_numpy(np.ascontiguousarray(np.asarray(x_local, np.float32)))
+    lo, hi = layer.token_range(M)
+    if x_local.shape[0] != hi - lo or x_local.shape[1] != routing.model.N:
+        raise ConfigurationError(f"x_local must be [{hi - lo}, {routing.model.N}] on rank {rank}, "
+                                 f"got {tuple(x_local.shape)}")
+    return layer.forward(x_local, ex, cw, M=M)

@@ -45,6 +45,15 @@ def main():
         torch.cuda.synchronize(dev)
         outs.append(y.float().cpu().numpy())
     assert all(np.array_equal(outs[0], o) for o in outs[1:]), "forwards differ across epochs"
+    # the reference-named per-rank entry point, with this rank's validated
+    # schedules, on the same layer: the same rows
+    from paper_2502_19811_b200 import (execute_scheduled_rank, meta_for_layer0, meta_for_layer1, resolve_layer0,
+                                       resolve_layer1)
+    s0 = resolve_layer0(routing, rank, meta_for_layer0(model, routing.workload))
+    s1 = resolve_layer1(routing, rank, meta_for_layer1(model, routing.workload))
+    y = execute_scheduled_rank(x[lo:hi], rw, routing, s0, s1, activation="tanh", combine_weights=cw, layer=layer)
+    torch.cuda.synchronize(dev)
+    assert np.array_equal(y.float().cpu().numpy(), outs[-1]), "execute_scheduled_rank differs from forward"
     parts = [None] * world
     dist.all_gather_object(parts, (lo, outs[-1]))
     if rank == 0:
