@@ -96,6 +96,13 @@ if life:
     print("CTA lifetime: entry first %+.1f last %+.1f us | exit first %+.1f last %+.1f us (rel. to first record)" % (
         (min(x[3] for x in life) - t0) / 1e3, (max(x[3] for x in life) - t0) / 1e3,
         (min(x[4] for x in life) - t0) / 1e3, (max(x[4] for x in life) - t0) / 1e3))
+if os.environ.get("TAIL"):
+    # the last epilogues: (cta, task, mma start/end, epilogue start/end)
+    mm = {(c, t): (s, e) for c, t, s, e in mma}
+    epi = sorted(by_role.get("epilogue", []), key=lambda x: x[3])[-int(os.environ["TAIL"]):]
+    for c, t, s, e in epi:
+        ms, me = mm.get((c & ~1, t), mm.get((c, t), (0, 0)))
+        print(f"  tail epi cta {c:3d} {kind(t)}#{t}: mma {ms/1e3:6.1f}-{me/1e3:6.1f}  epi {s/1e3:6.1f}-{e/1e3:6.1f}")
 comm = by_role.get("comm", [])
 if comm:
     print(f"  dispatch: {len(comm)} tiles, last published +{max(x[3] for x in comm)/1e3:.1f} us")
