@@ -787,7 +787,14 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   // the last layer1 units may run as 256-column halves (finer tail; off by
   // default: a half moves 64 B/cycle/SM for its MMAs instead of 48 and ran
   // ~35% slower per FLOP, tools/fused_timeline.py)
-  a.split_units = env_int("COMET_SPLIT1", 0);
+  // Default: long fold chains (top-k >= 4 with >= 4 hosted experts: the last
+  // units are folders reading up to k-1 rows each, 55-66 us epilogues at QW
+  // EP=8) end layer1 in 256-column halves over 3/4 of the pairs, so the
+  // folder epilogues split over twice the CTAs (QW EP=8 0.42 -> 0.40 ms;
+  // MX: halves only cost, 0.44 -> 0.47 ms at EP=8 -- off).
+  const int split_env = env_int("COMET_SPLIT1", -1);
+  a.split_units = split_env >= 0 ? split_env
+                  : (a.fuse_combine && c.topk >= 4 && x->E_r >= 4) ? 3 * (layer_grid(x) / 2) / 4 : 0;
   *out = a;
   return COMET_OK;
 }
