@@ -309,7 +309,7 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     (8, 3, 3000, 1024, 2048, "1", "2", "8"), (16, 4, 700, 512, 512, "1", "2", "2"),
     (16, 4, 700, 512, 512, "1", "0", "8"), (8, 2, 100, 512, 2048, "1", "2", "8"),
     (8, 1, 1000, 512, 1024, "1", "2", "0"), (8, 2, 6000, 1024, 3200, "1", "3", "8"),
-    (8, 2, 300, 512, 2048, "1", "0", "8")])
+    (8, 2, 300, 512, 2048, "1", "0", "8"), (8, 2, 1, 512, 1024, "1", "3", "8"), (8, 4, 129, 512, 512, "1", "1", "4")])
 def test_zerocopy_host_forward(E, topk, M, N, K, dedup, ilv, dl, monkeypatch):
     """comet_forward_zerocopy: dispatch CTAs read token rows from pinned host
     memory (once per token with dedup, fanned out to every hosted row), the
