@@ -162,14 +162,25 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
       const int n = re - rb;
       const int t = lane < n ? p.gather_row[padrow0 + rb + lane] : 0;
       const int src = src_rank_of(t, p.M, p.world);
+      // source ranks this item reads whose tokens are not known ready: every
+      // such flag polled at once, one lane each (one system-scope round trip
+      // instead of one per source rank)
+      unsigned long long need = 0;
+      for (int i = 0; i < n; ++i) need |= 1ull << __shfl_sync(0xffffffffu, src, i);
+      need &= ~ready_mask;
+      if (need) {
+        for (int r = lane; r < p.world; r += 32)
+          if ((need >> r) & 1) {
+            ptx::Spin sp;
+            while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + r), p.epoch)) sp.pause(64, 7);
+          }
+        __syncwarp();
+        ready_mask |= need;
+      }
       for (int i = 0; i < n; ++i) {
         const int ti = __shfl_sync(0xffffffffu, t, i);
         const int si = __shfl_sync(0xffffffffu, src, i);
         if (lane == 0) {
-          if (!((ready_mask >> si) & 1)) {
-            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.x_ready + si), p.epoch)) sp.pause(64, 7); }
-            ready_mask |= 1ull << si;
-          }
           if (p.chunk_ready && ti / p.chunk_tokens > chunk_ok) {  // chunks land in order
             const int c = ti / p.chunk_tokens;
             { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_sys(p.chunk_ready + c), p.epoch)) sp.pause(128, 8); }
