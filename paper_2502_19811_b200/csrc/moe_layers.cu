@@ -50,6 +50,9 @@ constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(2 * kTileRows, kHalfN);
 constexpr int kEpiThread0 = 128;                         // first epilogue thread
 constexpr uint32_t kSmemEpiWarp = 32 * 128;              // one warp's 32 rows x 64 columns (bf16)
 constexpr uint32_t kSmemEpi = 2 * 4 * kSmemEpiWarp;      // double-buffered, 4 epilogue warps
+// a dispatch CTA's ring + bookkeeping live in the same dynamic smem
+static_assert(comm::kRingBytes + sizeof(comm::CommSmem) <= kStages * kSmemStage + kSmemEpi,
+              "dispatch ring and its bookkeeping exceed the layer kernel's shared memory");
 
 struct Unit {
   int layer, pair, nb;
