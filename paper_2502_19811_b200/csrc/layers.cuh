@@ -3,6 +3,8 @@
 
 #include <cstdint>
 
+#include <cuda_bf16.h>
+
 #include "index.cuh"
 
 namespace comet {
