@@ -367,3 +367,27 @@ def test_dispatch_dedup_bitwise(E, topk, tp, ep, M, monkeypatch):
     silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
     ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), silu, cw, tp=tp)
     assert_close(outs[1], ref, what=f"dedup E={E} topk={topk} tp={tp} ep={ep}")
+
+
+@pytest.mark.parametrize("act", ["gelu_tanh", "relu", None])
+def test_zerocopy_unweighted_activations(act):
+    """Zero-copy host forward without combine weights (plain sum over the
+    token's experts, executor.py:102-120) and with each epilogue activation."""
+    import torch
+    model = ModelConfig(L=1, E=8, topk=2, N=512, K=1024)
+    par = ParallelSpec()
+    M = 2000
+    routing = build_routing(model, par, WorkloadSpec(M=M, seed=91, std=0.032))
+    w = random_weights(model, seed=92)
+    layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0), activation=act,
+                     knobs=LayerKnobs(n_comm0=16))
+    x = torch.from_numpy(np.random.default_rng(93).standard_normal((M, 512)).astype(np.float32)).to(torch.bfloat16)
+    ex = torch.from_numpy(routing.as_array().copy())
+    out = torch.empty(M, 512, dtype=torch.bfloat16).pin_memory()
+    layer.forward_host(x.pin_memory(), ex.pin_memory(), None, out=out)
+    torch.cuda.synchronize()
+    fns = {"gelu_tanh": lambda a: 0.5 * a * (1 + np.tanh(0.7978845608028654 * (a + 0.044715 * a ** 3))),
+           "relu": lambda a: np.maximum(a, 0.0), None: None}
+    ref = oracle_bf16_inputs(x.float().numpy(), w.w0, w.w1, routing.as_array(), fns[act])
+    assert_close(out.float().numpy(), ref, what=f"zero-copy unweighted act={act}")
+    layer.close()
