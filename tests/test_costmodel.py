@@ -54,3 +54,22 @@ def test_predict_split_answers_unprofiled_shapes():
     r1 = build_routing(model, ParallelSpec(1, 1), WorkloadSpec(M=4096, seed=0))
     cm = CM.preset()
     assert CM.simulate(r1, 0, cm, 2) == CM.simulate(r1, 0, cm, 64)
+
+
+def test_fold_loads_and_epilogue_fit():
+    """Fold counts per pair from the routing (a token's last hosted row folds
+    the others) and the epilogue / per-fold-row fit."""
+    qw = build_routing(ModelConfig(L=1, E=64, topk=8, N=3584, K=2560), ParallelSpec(1, 8), WorkloadSpec(M=8192, seed=0))
+    sh = CM.rank_shape(qw, 0)
+    assert [f for (j, _, _), f in zip(sh.pairs, sh.folds) if j == 7] == [7.0] * 4
+    assert all(f == 0.0 for (j, _, _), f in zip(sh.pairs, sh.folds) if j != 7)
+    mx = build_routing(ModelConfig(L=1, E=8, topk=2, N=4096, K=14336), ParallelSpec(1, 1), WorkloadSpec(M=4096, seed=0))
+    sh1 = CM.rank_shape(mx, 0)  # world 1: experts {2k, 2k+1} -> the odd expert's rows fold one row
+    assert all(f == (1.0 if j % 2 else 0.0) for (j, _, _), f in zip(sh1.pairs, sh1.folds))
+    rng = np.random.default_rng(1)
+    flops = rng.choice([1.07e9, 3.76e9], 200)
+    epi = [10e-6] * 50 + [10e-6 + 7 * 6e-6] * 20 + [5e-6 + 3.5 * 6e-6] * 10
+    cm = CM.fit([{"unit_flops": flops, "unit_s": 2e-6 + flops / 23e12, "cta_rates": [30e9], "fixed_s": 5e-5,
+                  "epi_s": epi, "epi_folds": [0] * 50 + [7] * 20 + [3.5] * 10, "epi_scale": [1] * 70 + [0.5] * 10}])
+    assert cm.epilogue_s == pytest.approx(10e-6) and cm.fold_row_s == pytest.approx(6e-6)
+    assert CM.default_split1(qw, 148) == 55 and CM.default_split1(mx, 148) == 0
