@@ -20,6 +20,7 @@ namespace comet {
 __global__ void index_build_kernel(IndexDev ix);
 __global__ void moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_b0,
                                  const __grid_constant__ CUtensorMap tm_a1, const __grid_constant__ CUtensorMap tm_b1,
+                                 const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
                                  const __grid_constant__ KernelArgs f);
 __global__ void combine_finish_kernel(const LayerArgs p, const __nv_bfloat16* cb, const uint32_t* cb_flag,
                                       const int32_t* experts);
@@ -172,6 +173,7 @@ struct comet_ctx {
   int32_t* routing = nullptr;
 
   CUtensorMap tm_xs, tm_H, tm_y, tm_xg;
+  CUtensorMap tm_Hs, tm_ys;  // epilogue TMA stores: box {64 cols, 32 rows} (one epilogue warp's block)
   unsigned long long* timeline = nullptr;
   int timeline_cap = 0;
   void* last_y = nullptr;
@@ -628,6 +630,8 @@ static int ensure_work(comet_ctx* x) {
   if (!rc) rc = make_map(&x->tm_xg, x->xg, x->cap_rows_pad, c.N, 128);
   if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
   if (!rc) rc = make_map(&x->tm_y, x->yrows, x->cap_rows_pad, c.N, 128);
+  if (!rc) rc = make_map(&x->tm_Hs, x->H, x->cap_rows_pad, x->k_local, 32);
+  if (!rc) rc = make_map(&x->tm_ys, x->yrows, x->cap_rows_pad, c.N, 32);
   return rc;
 }
 
@@ -711,7 +715,7 @@ static int launch_kernel(comet_ctx* x, KernelArgs& f, const CUtensorMap& a0, con
   at[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl_on(2) ? 2 : 1;
-  CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, a0, b0, a1, b1, f));
+  CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, a0, b0, a1, b1, x->tm_Hs, x->tm_ys, f));
   return COMET_OK;
 }
 

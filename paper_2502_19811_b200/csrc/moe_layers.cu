@@ -175,7 +175,8 @@ __device__ void download_rows(const KernelArgs& f, int did) {
 // (leader), warps 4-7 epilogue.
 __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem, const CUtensorMap* tm_a0,
                                              const CUtensorMap* tm_b0, const CUtensorMap* tm_a1,
-                                             const CUtensorMap* tm_b1) {
+                                             const CUtensorMap* tm_b1, const CUtensorMap* tm_s0,
+                                             const CUtensorMap* tm_s1) {
   uint8_t* epi_smem = smem + kStages * kSmemStage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi_smem + kSmemEpi);
   uint64_t* full = bars;
@@ -470,6 +471,9 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const unsigned long long my_addr = reinterpret_cast<unsigned long long>(my_dst);
       // 64 fp32 columns of this lane's row -> (fold) -> activation -> bf16 ->
       // coalesced stores
+      // contiguous destination rows (H, or yrows without the fused combine):
+      // TMA tensor stores; fused-combine units write scattered token rows
+      const bool tma_out = (w.layer == 0 || !p.fuse_combine) && !(p.debug & 16384);
       auto process = [&](int s, uint32_t (&v0)[32], uint32_t (&v1)[32]) {
         if (w.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
 #pragma unroll
@@ -514,10 +518,29 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // store instruction writes 4 whole 128 B lines (8 lanes per row).
         // Only this warp touches its staging rows: __syncwarp suffices.
         uint8_t* stg = epi_smem + ((s & 1) * 4 + ew) * kSmemEpiWarp;
+        // TMA store: the staging rows (SW128 layout) of chunk s-2 must be
+        // read out before they are overwritten
+        if (tma_out && s >= 2) {
+          if (lane == 0) ptx::bulk_wait_read<1>();
+          __syncwarp();
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        if (tma_out) {
+          // rows row0+32*ew.. are contiguous in H / yrows: one async 2D tensor
+          // store of the warp's 32 x 64 block (the swizzled staging layout is
+          // the map's SWIZZLE_128B box) instead of 8 transposed st.global
+          ptx::fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(w.layer ? tm_s1 : tm_s0, stg, w.nb * static_cast<int>(kBlockN) + col0 + s * 64,
+                              row0 + ew * 32);
+            ptx::bulk_commit();
+          }
+          return;
+        }
         __syncwarp();
         const int gsub = lane & 7, rsub = lane >> 3;
 #pragma unroll
@@ -584,6 +607,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (s * 64 >= cols_left || (p.debug & 64)) continue;
         process(s, v0, v1);
       }
+      if (tma_out) {  // this warp's tensor stores complete before the unit is counted
+        if (lane == 0) ptx::bulk_wait<0>();
+        __syncwarp();
+      }
       bool finisher = true;  // this CTA produces the tile's output (always, without split-K)
       if (S > 1) {
         // the last slice to land reduces all S partials in slice order
@@ -618,6 +645,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
               v1[i] = __float_as_uint(acc[32 + i]);
             }
             process(s, v0, v1);
+          }
+          if (tma_out) {
+            if (lane == 0) ptx::bulk_wait<0>();
+            __syncwarp();
           }
           if (threadIdx.x == kEpiThread0) p.split_cnt[split_tile] = 0u;  // ready for the next launch
         }
@@ -686,6 +717,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
 __global__ void __launch_bounds__(kThreads, 1)
 moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_b0,
                  const __grid_constant__ CUtensorMap tm_a1, const __grid_constant__ CUtensorMap tm_b1,
+                 const __grid_constant__ CUtensorMap tm_s0, const __grid_constant__ CUtensorMap tm_s1,
                  const __grid_constant__ KernelArgs f) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_last;
@@ -719,7 +751,7 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
       compute = false;
     }
   }
-  if (compute) compute_role(f, smem, &tm_a0, &tm_b0, &tm_a1, &tm_b1);
+  if (compute) compute_role(f, smem, &tm_a0, &tm_b0, &tm_a1, &tm_b1, &tm_s0, &tm_s1);
 
   // The last CTA out resets the launch's claim counter and H-tile counters
   // (nothing reads them after every CTA has left).
