@@ -36,8 +36,10 @@ struct LayerArgs {
   float* part;            // split-K fp32 partials [tiles*NB][S][128][512] (<= pairs*2 CTA tiles)
   uint32_t* split_cnt;    // [tiles*NB] slices landed (reset by the finisher)
   uint32_t epoch;
-  int debug;              // bit0: comm CTAs idle; bit2: spin waits; bit3: no MMA; bit4: no loads;
-                          // bit5: sequential (GEMMs start after the whole dispatch); bit6/7: no stores / no drain
+  int debug;              // COMET_DEBUG bits (timing experiments, wrong results unless noted):
+                          // 1: comm CTAs idle; 8: no MMA; 16: no loads; 32: sequential (GEMMs start
+                          // after the whole dispatch; correct, the cli baseline); 64/128: no stores /
+                          // no drain; 16384: st.global epilogue instead of TMA stores (correct)
 
   // index (device)
   const int32_t* meta;
