@@ -40,6 +40,19 @@ def configs(quick):
     return out
 
 
+SPEC_BF16_TFLOPS = 2250.0  # nominal dense bf16 (B200 spec sheet), labelled as such
+
+
+def extra_terms(routing, latency_ms, hbm_gbs):
+    """SURVEY §8(d)'s secondary terms: the spec-peak roofline variant and the
+    weight-streaming time max_r(E_r * 2 * N * K/tp * 2 B) / HBM."""
+    model, par = routing.model, routing.parallel
+    rf = roofline(routing, SPEC_BF16_TFLOPS)
+    w_bytes = (model.E // par.ep) * 2 * model.N * (model.K // par.tp) * 2
+    return {"roofline_ms_spec_2250tf": round(rf.ms, 4), "pct_roofline_spec": round(100 * rf.ms / latency_ms, 1),
+            "t_weights_hbm_ms": round(w_bytes / (hbm_gbs * 1e9) * 1e3, 4)}
+
+
 def unfused_ms(grp, iters=10):
     from paper_2502_19811_b200.unfused import UnfusedLayer
     l = grp.layers[0]
@@ -68,7 +81,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--nc0", default="16,32,64", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
     a = ap.parse_args()
-    burst, sust, _, src = load_peaks()
+    burst, sust, hbm, src = load_peaks()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as fh:
         for shape, ep, tp, M, std in configs(a.quick):
@@ -95,6 +108,7 @@ def main():
                    "pct_roofline_burst": round(100 * rf_b.ms / best["latency_ms"], 1),
                    "pct_roofline_sustained": round(100 * rf_s.ms / best["latency_ms"], 1),
                    "peaks": {"burst_tflops": burst, "sustained_tflops": sust, "source": src}}
+            rec.update(extra_terms(routing, rec["latency_ms"], hbm))
             if par.world_size == 1:
                 try:
                     u = unfused_ms(grp)
