@@ -382,6 +382,7 @@ def run_ours(args):
             "pct_of_roofline": round(100.0 * t_flops_ms / ms, 2),
             "roofline_ms": round(t_flops_ms, 4),
             "pct_of_roofline_sustained": round(100.0 * t_flops_sust_ms / ms, 2),
+            "pct_of_roofline_spec_2250tf": round(100.0 * t_flops_ms * peak_burst / 2250.0 / ms, 2),
             "roofline_note": "roofline_ms = 2 GEMMs x 2*rows*N*K/tp FLOP at the measured burst bf16 peak "
                              "(BASELINE.md); pct_of_roofline_sustained uses the measured sustained peak",
             "roofline": {"bound": "tensor",
