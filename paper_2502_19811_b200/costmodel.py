@@ -45,6 +45,7 @@ from .routing import RoutingTable, build_routing
 PAIR_ROWS = 256
 BLOCK_N = 512
 HALF_N = 256
+HALF_COST = 1.35  # a 256-column half unit's time per FLOP vs a full unit (64 vs 48 B/cycle/SM of operands)
 ITEM_ROWS = 32
 PRESET_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "costmodel_b200.json")
 
@@ -201,6 +202,8 @@ def _units(shape: RankShape, group: int, wave: int, split1: int = 0, n_pairs: in
                 for p in range(g0, g0 + ge):
                     seq1.append((1, p, min(BLOCK_N, shape.n_embed - nb * BLOCK_N), 1, 0))
     S1 = _ksplit(len(seq1), shape.k_local // 64, n_pairs)
+    if split1 < 0:  # automatic (sched.cuh seq_total): a 1-4 round layer1 ends its last 16 units in halves
+        split1 = 16 if n_pairs < len(seq1) < 4 * n_pairs else 0
     seq1 = _sliced(seq1, S1) if S1 > 1 else _halves(seq1, split1)
     return seq + seq1, nb0
 
@@ -208,10 +211,10 @@ def _units(shape: RankShape, group: int, wave: int, split1: int = 0, n_pairs: in
 def default_split1(routing: RoutingTable, blocks: int) -> int:
     """The kernel's default layer1 tail halves (capi.cu layer1_args): 3/4 of
     the pairs when fold chains are long (world > 1, top-k >= 4, >= 4 hosted
-    experts), else none."""
+    experts), else automatic (-1: 16 units when layer1 is 1-4 rounds)."""
     par, model = routing.parallel, routing.model
     long_folds = par.world_size > 1 and model.topk >= 4 and model.E // par.ep >= 4
-    return 3 * (blocks // 2) // 4 if long_folds else 0
+    return 3 * (blocks // 2) // 4 if long_folds else -1  # -1: by the round count (_units)
 
 
 def simulate(routing: RoutingTable, rank: int, cm: CostModel, n_c: int, group: int = 4, wave: int = 4) -> float:
@@ -246,7 +249,8 @@ def simulate(routing: RoutingTable, rank: int, cm: CostModel, n_c: int, group: i
         rows = PAIR_ROWS
         k = shape.n_embed if layer == 0 else shape.k_local
         eff_cols = HALF_N if cols <= HALF_N else BLOCK_N
-        dur = cm.unit_s(2.0 * rows * eff_cols * k / S) + cm.epilogue_s * eff_cols / BLOCK_N
+        cost_cols = HALF_N * HALF_COST if cols <= HALF_N else BLOCK_N
+        dur = cm.unit_s(2.0 * rows * cost_cols * k / S) + cm.epilogue_s * eff_cols / BLOCK_N
         if S > 1:  # fp32 partial store (2x the bytes); the last slice reduces all S
             dur += cm.epilogue_s * (1 + (S if ks == S - 1 else 0))
         if layer == 1 and fused:
@@ -331,7 +335,7 @@ def sample_from_timeline(records: Iterable[Tuple[int, str, int, int, int]], rout
         if cols <= 0:
             continue
         k = shape.n_embed if layer == 0 else shape.k_local
-        eff = HALF_N if cols <= HALF_N else BLOCK_N
+        eff = HALF_N * HALF_COST if cols <= HALF_N else BLOCK_N
         s0 = max(s, load.get((c, t), s))  # dependency waits excluded
         uf.append(2.0 * PAIR_ROWS * eff * k / S)
         us.append((e - s0) * 1e-9)

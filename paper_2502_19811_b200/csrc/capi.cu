@@ -798,7 +798,8 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   // MX: halves only cost, 0.44 -> 0.47 ms at EP=8 -- off).
   const int split_env = env_int("COMET_SPLIT1", -1);
   a.split_units = split_env >= 0 ? split_env
-                  : (a.fuse_combine && c.topk >= 4 && x->E_r >= 4) ? 3 * (layer_grid(x) / 2) / 4 : 0;
+                  : (a.fuse_combine && c.topk >= 4 && x->E_r >= 4) ? 3 * (layer_grid(x) / 2) / 4
+                  : env_int("COMET_SPLIT1_AUTO", 1) ? -1 : 0;  // -1: sched.cuh picks by the round count
   *out = a;
   return COMET_OK;
 }

@@ -115,7 +115,14 @@ COMET_HD int seq_total(const KernelArgs& f, int P, int n_pairs, Sched& s0, Sched
     const int U0 = P * f.l[0].n_blocks;
     s0 = make_sched(U0, f.l[0].split_tail ? layer0_split(U0, n_pairs) : 0, ksplit_for(f.l[0], P, n_pairs));
   }
-  if (f.mode != 0) s1 = make_sched(P * f.l[1].n_blocks, f.l[1].split_units, ksplit_for(f.l[1], P, n_pairs));
+  if (f.mode != 0) {
+    const int U1 = P * f.l[1].n_blocks;
+    // split_units < 0: automatic -- a layer1 of 1-4 rounds ends its last 16
+    // units in halves (the partial last round balances better), else none
+    const int split1 = f.l[1].split_units >= 0 ? f.l[1].split_units
+                       : (U1 > n_pairs && U1 < 4 * n_pairs) ? 16 : 0;
+    s1 = make_sched(U1, split1, ksplit_for(f.l[1], P, n_pairs));
+  }
   return s0.total + s1.total;
 }
 

@@ -72,4 +72,4 @@ def test_fold_loads_and_epilogue_fit():
     cm = CM.fit([{"unit_flops": flops, "unit_s": 2e-6 + flops / 23e12, "cta_rates": [30e9], "fixed_s": 5e-5,
                   "epi_s": epi, "epi_folds": [0] * 50 + [7] * 20 + [3.5] * 10, "epi_scale": [1] * 70 + [0.5] * 10}])
     assert cm.epilogue_s == pytest.approx(10e-6) and cm.fold_row_s == pytest.approx(6e-6)
-    assert CM.default_split1(qw, 148) == 55 and CM.default_split1(mx, 148) == 0
+    assert CM.default_split1(qw, 148) == 55 and CM.default_split1(mx, 148) == -1
