@@ -1110,13 +1110,14 @@ int comet_forward_zerocopy(comet_ctx* x, const void* h_x, const int32_t* h_exper
   f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
   f.l[1].fuse_combine = 1;
   if (x->E_r == 1 || c.topk == 1 || tile_order) f.l[1].pairs = x->ix.pairs0;
-  // Interleave the layers (COMET_ZC_ILV groups of lag; 0 = layer1 after all
+  // Interleave the layers (COMET_ZC_ILV groups of lag, default 1 with the
+  // 16-pair groups the host layer passes; 0 = layer1 after all
   // of layer0): the dispatch is PCIe-paced, so layer0 alone leaves the
   // tensor cores waiting; layer1 groups of finished pairs fill the gaps and
   // start the host writes early.  Needs one pair order for both layers: at
   // world 1 the claim order is expert-ascending like pairs1 (no fold-level
   // order), and no split tails / split-K.
-  f.interleave = fold_order ? 0 : env_int("COMET_ZC_ILV", 3);
+  f.interleave = fold_order ? 0 : env_int("COMET_ZC_ILV", 1);
   if (f.interleave > 0) {
     f.l[1].pairs = x->ix.pairs0;
     f.l[1].order_group2 = f.l[0].order_group;

@@ -281,9 +281,12 @@ class MoELayer:
             cw = None if combine_w is None else combine_w.float().contiguous()
             xb = x_host if x_host.dtype == torch.bfloat16 else x_host.to(torch.bfloat16)
             k = self.knobs
+            # 16-pair groups, layer1 one group behind (PCIe-paced dispatch: a
+            # group spans two experts' tiles, whose token rows land together
+            # with the per-token dedup; 3.50 -> 3.40 ms vs 8-pair groups, lag 3)
             self.ctx.forward_zerocopy(xb.contiguous(), ex.contiguous(), cw, out, M, self.weights.w0t,
                                       self.weights.w1t, self.act, n_comm0=int(os.environ.get("COMET_ZC_NC", 16)),
-                                      group0=k.group0, wave1=k.wave1)
+                                      group0=int(os.environ.get("COMET_ZC_G0", 16)), wave1=k.wave1)
             return out
         if (world == 1 and chunks is None and e2e_mode == "stream"
                 and self.n_pad == N and x_host.is_pinned() and out.is_pinned() and out.is_contiguous()):

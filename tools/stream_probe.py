@@ -69,7 +69,7 @@ if comm:
           f"100% {comm[-1][2]:.0f} us")
 P = int(layer.ctx.index_meta()[3])
 U0 = P * 28
-ilv = int(os.environ.get("COMET_ZC_ILV", 3)) if mode == "zc" else 0
+ilv = int(os.environ.get("COMET_ZC_ILV", 1)) if mode == "zc" else 0
 
 
 def seq_layer(g):
