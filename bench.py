@@ -171,20 +171,27 @@ def cpu_reference_sample(model, routing, sample_tokens: int, steps: int, warmup:
     w1 = rng.standard_normal((model.E, model.K, model.N), dtype=np.float32) / np.float32(math.sqrt(model.N))
     x = rng.standard_normal((sample_tokens, model.N), dtype=np.float32)
     ex = routing.as_array()[:sample_tokens]
-    for _ in range(max(0, warmup)):
-        O.layer_forward(x, w0, w1, ex, dtype=np.float32)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        O.layer_forward(x, w0, w1, ex, dtype=np.float32)
-        times.append(time.perf_counter() - t0)
+    # every host core for the BLAS pool (torchrun exports OMP_NUM_THREADS=1 to
+    # multi-rank jobs, which OpenBLAS would otherwise honour)
+    import contextlib
+    limits, threads = contextlib.nullcontext(), os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        n_host = len(os.sched_getaffinity(0))
+        limits = threadpool_limits(limits=n_host, user_api="blas")
+        threads = max([i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"] or [n_host])
+    except Exception:
+        pass
+    with limits:
+        for _ in range(max(0, warmup)):
+            O.layer_forward(x, w0, w1, ex, dtype=np.float32)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.layer_forward(x, w0, w1, ex, dtype=np.float32)
+            times.append(time.perf_counter() - t0)
     scale = routing.workload.M / sample_tokens
     ms = statistics.median(times) * 1e3 * scale
-    try:
-        import torch
-        threads = torch.get_num_threads()
-    except Exception:
-        threads = os.cpu_count()
     return ms, {"cores": os.cpu_count(), "threads": threads,
                 "sample": f"{sample_tokens} of {routing.workload.M} tokens (all experts, full N/K), fp32 numpy "
                           f"(OpenBLAS), median of {steps} steps, scaled x{scale:g} to the full workload"}
