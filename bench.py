@@ -261,7 +261,11 @@ def run_ours(args):
     routing = build_routing(model, par, WorkloadSpec(M=args.M, seed=0, std=args.std))
     M = args.M
     dev = torch.device("cuda", local)
-    knobs = LayerKnobs(n_comm0=args.n_comm0, n_comm1=args.n_comm1,
+    # the dispatch CTAs must leave compute pairs: a reduced grid (COMET_GRID,
+    # the ranks-sharing-one-GPU test mode) caps them at half of it
+    grid = int(os.environ.get("COMET_GRID", torch.cuda.get_device_properties(local).multi_processor_count))
+    n_comm0 = max(2, min(args.n_comm0, (grid // 2) // 2 * 2))
+    knobs = LayerKnobs(n_comm0=n_comm0, n_comm1=args.n_comm1,
                        group0=args.group0, wave1=args.wave1)
     weights = rank_weights_random(model, par, rank, dev)
     layer = distributed.init_layer(model, par, M, weights, knobs=knobs) if world > 1 else \
