@@ -463,7 +463,10 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.group0 is None:
-        args.group0 = 8 if args.gpus == 1 else 4
+        # measured (tools/gpu_runs/gpu_run105.sh, 3 reps): 8-pair groups win at
+        # EP=1 and EP=8 (all 8 pairs of a rank in one group: 0.423 -> 0.417 ms),
+        # 4-pair groups at EP=2/4 (1.386 vs 1.404, 0.737 vs 0.744 ms)
+        args.group0 = 8 if args.gpus == 1 or args.gpus >= 8 else 4
     return run_reference(args) if args.impl == "reference" else run_ours(args)
 
 
