@@ -454,7 +454,7 @@ def main():
     ap.add_argument("--n-comm0", type=int, default=64)
     ap.add_argument("--n-comm1", type=int, default=0)
     ap.add_argument("--group0", type=int, default=None,
-                    help="layer0 pair-group raster (default: 8 on one GPU, 4 for EP > 1; measured)")
+                    help="layer0 pair-group raster (default: 8 at EP=1 and EP>=8, 4 at EP=2/4; measured)")
     ap.add_argument("--wave1", type=int, default=4)
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
