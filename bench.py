@@ -451,7 +451,8 @@ def main():
     ap.add_argument("--shape", choices=sorted(SHAPES), default="mixtral-8x7b")
     ap.add_argument("--M", type=int, default=8192)
     ap.add_argument("--std", type=float, default=0.0)
-    ap.add_argument("--n-comm0", type=int, default=64)
+    ap.add_argument("--n-comm0", type=int, default=None,
+                    help="layer0 dispatch CTAs (default 8 per rank of the group, max 64: measured best at EP=2/4/8)")
     ap.add_argument("--n-comm1", type=int, default=0)
     ap.add_argument("--group0", type=int, default=None,
                     help="layer0 pair-group raster (default: 8 at EP=1 and EP>=8, 4 at EP=2/4; measured)")
@@ -462,6 +463,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.n_comm0 is None:
+        # measured (gpu_run106.sh, tools/matrix.py): EP=2 16 vs 64 CTAs
+        # 1.396 vs 1.409 ms, EP=4 32 vs 64 0.734 vs 0.742 ms, EP=8 64 best
+        args.n_comm0 = min(64, 8 * args.gpus)
     if args.group0 is None:
         # measured (tools/gpu_runs/gpu_run105.sh, 3 reps): 8-pair groups win at
         # EP=1 and EP=8 (all 8 pairs of a rank in one group: 0.423 -> 0.417 ms),
