@@ -153,6 +153,13 @@ class LayerKnobs:
     group0: int = 4
     wave1: int = 4
 
+    @classmethod
+    def for_world(cls, world: int) -> "LayerKnobs":
+        """Measured defaults (bench.py / tools/gpu_runs/gpu_run105-106.sh): 8
+        dispatch CTAs per rank of the group (max 64); 8-pair layer0 groups at
+        EP=1 and EP>=8, 4-pair groups at EP=2/4."""
+        return cls(n_comm0=min(64, 8 * max(1, world)), group0=8 if world == 1 or world >= 8 else 4)
+
 
 class MoELayer:
     """One rank's fused MoE layer forward on its GPU.
@@ -176,7 +183,7 @@ class MoELayer:
         self.torch = self.ctx.torch
         self.weights = weights
         self.act = activation_code(activation)
-        self.knobs = knobs or LayerKnobs()
+        self.knobs = knobs or LayerKnobs.for_world(parallel.world_size)
         self.device = device
         self._xbuf = self.ctx.token_buffer()
 

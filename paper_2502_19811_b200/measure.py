@@ -121,7 +121,7 @@ class EmulatedGroup:
                 w0t[e, :kl, :model.N] = (torch.randn(kl, model.N, device="cuda", generator=g) * s).to(torch.bfloat16)
                 w1t[e, :model.N, :kl] = (torch.randn(model.N, kl, device="cuda", generator=g) * s).to(torch.bfloat16)
             self.layers.append(MoELayer(model, parallel, r, max(1, M), RankWeights(w0t, w1t),
-                                        activation=activation, knobs=knobs or LayerKnobs()))
+                                        activation=activation, knobs=knobs or LayerKnobs.for_world(W)))
         if W > 1:
             _lib.Context.link_local([l.ctx for l in self.layers])
         x = torch.randn(M, model.N, device="cuda", generator=g).to(torch.bfloat16)
