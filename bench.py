@@ -192,7 +192,12 @@ def cpu_reference_sample(model, routing, sample_tokens: int, steps: int, warmup:
             times.append(time.perf_counter() - t0)
     scale = routing.workload.M / sample_tokens
     ms = statistics.median(times) * 1e3 * scale
-    return ms, {"cores": os.cpu_count(), "threads": threads,
+    try:
+        import torch
+        torch_threads = torch.get_num_threads()
+    except Exception:
+        torch_threads = None
+    return ms, {"cores": os.cpu_count(), "threads": threads, "torch_threads": torch_threads,
                 "sample": f"{sample_tokens} of {routing.workload.M} tokens (all experts, full N/K), fp32 numpy "
                           f"(OpenBLAS), median of {steps} steps, scaled x{scale:g} to the full workload"}
 
@@ -213,7 +218,8 @@ def run_reference(args):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args, model, ep, tp),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": info["threads"], "kind": "port",
-                         "sample": info["sample"]},
+                         "sample": info["sample"], "host_cpu_count": info["cores"], "blas_threads": info["threads"],
+                         "torch_threads": info["torch_threads"]},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
@@ -387,7 +393,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cms, info = cpu_reference_sample(model, routing, args.cpu_sample, 3, 1)
         cpu = {"value": round(cms, 3), "unit": "ms", "cores": info["threads"], "kind": "port",
-               "sample": info["sample"]}
+               "sample": info["sample"], "host_cpu_count": info["cores"], "blas_threads": info["threads"],
+               "torch_threads": info["torch_threads"]}
 
     if rank == 0:
         out = {
