@@ -212,6 +212,70 @@ int comet_router_topk(const void* d_logits, int logits_dtype, int M, int E, int 
 /* Number of SMs and max co-resident 2-CTA clusters for the layer kernel. */
 int comet_device_info(int device, int32_t out[4]);
 
+/* Per-context kernel options (the knobs that are not call arguments).
+ * Every option has a measured default; nothing is read from the
+ * environment.  comet_set_option(ctx, opt, COMET_OPT_DEFAULT) restores the
+ * default.  Options take effect at the next launch on the context.
+ *   FUSED          1: both layers in one persistent launch (default 1)
+ *   KSPLIT_MAX     split-K slices when a layer has fewer tiles than pairs,
+ *                  0..8 (default 8)
+ *   SPLIT_TAIL0    layer0's last partial round as 256-column halves (1)
+ *   SPLIT1         layer1 units run as halves at the end: -1 automatic by
+ *                  shape (default), 0 none, n the last n units
+ *   DEDUP          world > 1: per-(token, rank) deduplicated NVLink pulls,
+ *                  -1 automatic (default: on when a token can have several
+ *                  hosted rows on a rank), 0 off, 1 on
+ *   PULL_LOCAL     world > 1: dispatch CTAs place the local rows too (1)
+ *   FOLD_ORDER     world > 1: layer1 pairs in fold-level order (1)
+ *   GROUP1         layer1 pair-group size, 0 = layer0's group (0)
+ *   CHUNK_ROWS     dispatch item rows 1..32 (32)
+ *   PDL            programmatic dependent launch bitmask: 1 local dispatch,
+ *                  2 layer kernel, 4 combine kernels (6)
+ *   GRID           cap on the persistent grid in CTAs, 0 = every SM (0)
+ *   FUSE1          world 1: fused epilogue combine instead of the combine
+ *                  kernel (0)
+ *   SPIN_TIMEOUT_MS  device flag waits trap after this long (600000 = 10
+ *                  min; a straggling peer must not kill the job)
+ *   ZC_DEDUP / ZC_INTERLEAVE / ZC_DOWNLOAD / ZC_ORDER / ZC_FOLD_ORDER
+ *                  zero-copy forward: per-token PCIe dedup (1), layer1
+ *                  groups interleaved at this lag (1), dispatch CTAs that
+ *                  download the output (8), (row tile, expert) pair order
+ *                  (0), fold-level order (0)
+ *   STREAM_FUSE    streamed host forward: epilogue fold instead of the
+ *                  dispatch-CTA combine (0)
+ *   SEQUENTIAL     no overlap: layer0 GEMMs start after the WHOLE dispatch
+ *                  (the all-to-all-then-GroupGEMM baseline of the cli; 0) */
+#define COMET_OPT_FUSED 0
+#define COMET_OPT_KSPLIT_MAX 1
+#define COMET_OPT_SPLIT_TAIL0 2
+#define COMET_OPT_SPLIT1 3
+#define COMET_OPT_DEDUP 4
+#define COMET_OPT_PULL_LOCAL 5
+#define COMET_OPT_FOLD_ORDER 6
+#define COMET_OPT_GROUP1 7
+#define COMET_OPT_CHUNK_ROWS 8
+#define COMET_OPT_PDL 9
+#define COMET_OPT_GRID 10
+#define COMET_OPT_FUSE1 11
+#define COMET_OPT_SPIN_TIMEOUT_MS 12
+#define COMET_OPT_ZC_DEDUP 13
+#define COMET_OPT_ZC_INTERLEAVE 14
+#define COMET_OPT_ZC_DOWNLOAD 15
+#define COMET_OPT_ZC_ORDER 16
+#define COMET_OPT_ZC_FOLD_ORDER 17
+#define COMET_OPT_STREAM_FUSE 18
+#define COMET_OPT_SEQUENTIAL 19
+#define COMET_OPT_COUNT 20
+#define COMET_OPT_DEFAULT (-2147483647 - 1)
+int comet_set_option(comet_ctx* ctx, int opt, int value);
+int comet_get_option(comet_ctx* ctx, int opt, int* value);
+
+/* Host-side abort of device waits: a non-zero value makes every kernel of
+ * this process that is spinning on a peer flag trap at its next timeout
+ * check (about every 64 polls) instead of waiting out SPIN_TIMEOUT_MS --
+ * for a watchdog that knows a peer is gone.  0 clears it. */
+int comet_abort_waits(int value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcomet_b200.so")
 SOURCES = ["index_build.cu", "moe_layers.cu", "router.cu", "capi.cu"]
-HEADERS = ["ptx.cuh", "index.cuh", "layers.cuh", "comm.cuh"]
+HEADERS = ["ptx.cuh", "index.cuh", "layers.cuh", "comm.cuh", "sched.cuh"]
 
 
 def nvcc() -> str:

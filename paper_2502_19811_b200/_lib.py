@@ -33,7 +33,16 @@ EXPORTS = (
     "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_layers", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
     "comet_timeline_enable", "comet_timeline_dump", "comet_router_topk", "comet_forward_host", "comet_forward_zerocopy",
+    "comet_set_option", "comet_get_option", "comet_abort_waits",
 )
+
+# Per-context kernel options (include/comet_b200.h COMET_OPT_*).
+OPTIONS = {
+    "fused": 0, "ksplit_max": 1, "split_tail0": 2, "split1": 3, "dedup": 4, "pull_local": 5, "fold_order": 6,
+    "group1": 7, "chunk_rows": 8, "pdl": 9, "grid": 10, "fuse1": 11, "spin_timeout_ms": 12, "zc_dedup": 13,
+    "zc_interleave": 14, "zc_download": 15, "zc_order": 16, "zc_fold_order": 17, "stream_fuse": 18, "sequential": 19,
+}
+OPT_DEFAULT = -2147483648
 ROLES = ("load", "mma", "tmem_wait", "epilogue", "comm")
 
 
@@ -102,6 +111,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_router_topk": ([vp, i32, i32, i32, i32, i32, vp, vp, vp], i32),
         "comet_forward_host": ([vp, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, i32, vp], i32),
         "comet_forward_zerocopy": ([vp, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, vp], i32),
+        "comet_set_option": ([vp, i32, i32], i32),
+        "comet_get_option": ([vp, i32, c.POINTER(i32)], i32),
+        "comet_abort_waits": ([i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -127,6 +139,13 @@ def require_device():
         raise NativeUnavailable("no CUDA device visible: the fused MoE layer runs only on sm_100a GPUs")
     load()
     return torch
+
+
+def abort_waits(value: int = 1) -> None:
+    """Make every device flag wait of this process trap at its next check
+    (comet_abort_waits): for a watchdog that knows a peer rank is gone.
+    ``abort_waits(0)`` clears it."""
+    check(load().comet_abort_waits(int(value)))
 
 
 def device_info(device: int = 0) -> Dict[str, int]:
@@ -171,6 +190,19 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    # -- options ------------------------------------------------------------
+    def set_option(self, name: str, value) -> None:
+        """Set a COMET_OPT_* option (None restores the library default)."""
+        if name not in OPTIONS:
+            raise ConfigurationError(f"unknown option {name!r}; choose from {sorted(OPTIONS)}")
+        v = OPT_DEFAULT if value is None else int(value)
+        check(self.lib.comet_set_option(self.handle, OPTIONS[name], v))
+
+    def get_option(self, name: str) -> int:
+        out = ctypes.c_int()
+        check(self.lib.comet_get_option(self.handle, OPTIONS[name], ctypes.byref(out)))
+        return out.value
 
     # -- buffers ------------------------------------------------------------
     def _view(self, ptr: int, shape, dtype):

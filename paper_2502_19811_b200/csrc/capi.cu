@@ -66,21 +66,21 @@ constexpr size_t kIndexSmem = 8192 * sizeof(long long);
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
+// Option defaults (comet_b200.h COMET_OPT_*), all measured (DESIGN.md §4/§6).
+// PDL default 6: with bit 1 the host-pipeline test (forward_host, uneven
+// token chunks) read a previous chunk's index in dispatch_local -- kept off.
+constexpr int kOptDefaults[COMET_OPT_COUNT] = {
+    /*FUSED*/ 1, /*KSPLIT_MAX*/ 8, /*SPLIT_TAIL0*/ 1, /*SPLIT1*/ -1, /*DEDUP*/ -1, /*PULL_LOCAL*/ 1,
+    /*FOLD_ORDER*/ 1, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 6, /*GRID*/ 0, /*FUSE1*/ 0,
+    /*SPIN_TIMEOUT_MS*/ 600000, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
+    /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0};
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous one drains; it calls griddepcontrol.wait before touching
-// the previous kernel's results.  COMET_PDL=0 launches normally.
-// COMET_PDL bitmask: 1 dispatch_local, 2 layer kernel, 4 combine kernels.
-// Default 6: with bit 1 the host-pipeline test (forward_host, uneven token
-// chunks) read a previous chunk's index in dispatch_local -- kept off.
-bool pdl_on(int bit) { return (env_int("COMET_PDL", 6) & bit) != 0; }
-
+// the previous kernel's results.  `pdl` is the context's PDL bitmask
+// (COMET_OPT_PDL): 1 dispatch_local, 2 layer kernel, 4 combine kernels.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(int bit, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+cudaError_t launch_pdl(int pdl, int bit, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
@@ -91,7 +91,7 @@ cudaError_t launch_pdl(int bit, void (*kernel)(KArgs...), dim3 grid, dim3 block,
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = pdl_on(bit) ? 1 : 0;
+  lc.numAttrs = (pdl & bit) ? 1 : 0;
   return cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
 }
 
@@ -116,8 +116,7 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  if (const char* e = getenv("COMET_L2PROMO")) promo = static_cast<CUtensorMapL2promotion>(atoi(e));
+  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -136,6 +135,7 @@ struct MapCache {
 
 struct comet_ctx {
   comet_config cfg;
+  int opt[COMET_OPT_COUNT];  // COMET_OPT_* values (kOptDefaults until set)
   int e_lo = 0, E_r = 0, k_local = 0, n_sm = 0, max_clusters = 0;
   int nb0 = 0, nb1 = 0, kb0 = 0, kb1 = 0;
   uint32_t epoch = 0;
@@ -192,7 +192,72 @@ struct comet_ctx {
   int n_h = 0;
 };
 
+cudaError_t set_abort_flag_index(const volatile uint32_t* p);
+cudaError_t set_abort_flag_layers(const volatile uint32_t* p);
+
+namespace {
+
+uint32_t* g_abort_host = nullptr;  // pinned, mapped (comet_abort_waits)
+
+// Device flag-wait timeout of this context's device (ptx::Spin; both
+// translation units hold their own copy of the timeout and abort pointer).
+int apply_spin_timeout(comet_ctx* x) {
+  const unsigned long long ms = static_cast<unsigned long long>(std::max(1, x->opt[COMET_OPT_SPIN_TIMEOUT_MS]));
+  CK(cudaSetDevice(x->cfg.device));
+  CK(set_spin_timeout_index(ms * 1000000ull));
+  CK(set_spin_timeout_layers(ms * 1000000ull));
+  // process-wide host abort word (comet_abort_waits), mapped into every device
+  if (!g_abort_host) {
+    CK(cudaHostAlloc(&g_abort_host, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    *g_abort_host = 0;
+  }
+  uint32_t* dev = nullptr;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), g_abort_host, 0));
+  CK(set_abort_flag_index(dev));
+  CK(set_abort_flag_layers(dev));
+  return COMET_OK;
+}
+
+// DEDUP -1 (automatic): off -- measured slower in single-GPU emulation for
+// every BASELINE shape; 1 forces it on.
+bool dedup_on(const comet_ctx* x) { return x->opt[COMET_OPT_DEDUP] > 0; }
+
+int group1(const comet_ctx* x, int group0) { return x->opt[COMET_OPT_GROUP1] > 0 ? x->opt[COMET_OPT_GROUP1] : group0; }
+
+}  // namespace
+
 extern "C" {
+
+int comet_set_option(comet_ctx* x, int opt, int value) {
+  if (!x) return fail(COMET_EINVAL, "null context");
+  if (opt < 0 || opt >= COMET_OPT_COUNT) return fail(COMET_EINVAL, "unknown option %d", opt);
+  if (value == COMET_OPT_DEFAULT) value = kOptDefaults[opt];
+  if (opt == COMET_OPT_CHUNK_ROWS && (value < 1 || value > 32))
+    return fail(COMET_EINVAL, "CHUNK_ROWS must be in [1, 32], got %d", value);
+  if (opt == COMET_OPT_KSPLIT_MAX && (value < 0 || value > 8))
+    return fail(COMET_EINVAL, "KSPLIT_MAX must be in [0, 8], got %d", value);
+  if (opt == COMET_OPT_GRID && (value < 0 || value == 1 || (value & 1)))
+    return fail(COMET_EINVAL, "GRID must be 0 or an even CTA count >= 2, got %d", value);
+  if (opt == COMET_OPT_SPIN_TIMEOUT_MS && value < 1)
+    return fail(COMET_EINVAL, "SPIN_TIMEOUT_MS must be >= 1, got %d", value);
+  const int old = x->opt[opt];
+  x->opt[opt] = value;
+  if (opt == COMET_OPT_SPIN_TIMEOUT_MS && old != value) return apply_spin_timeout(x);
+  return COMET_OK;
+}
+
+int comet_get_option(comet_ctx* x, int opt, int* value) {
+  if (!x || !value) return fail(COMET_EINVAL, "null argument");
+  if (opt < 0 || opt >= COMET_OPT_COUNT) return fail(COMET_EINVAL, "unknown option %d", opt);
+  *value = x->opt[opt];
+  return COMET_OK;
+}
+
+int comet_abort_waits(int value) {
+  if (!g_abort_host) return fail(COMET_EINVAL, "no context created yet");
+  *reinterpret_cast<volatile uint32_t*>(g_abort_host) = static_cast<uint32_t>(value);
+  return COMET_OK;
+}
 
 const char* comet_last_error(void) { return g_err.c_str(); }
 int comet_version(void) { return 1; }
@@ -258,11 +323,10 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
   comet_ctx* x = new comet_ctx();
   x->cfg = c;
   CK(cudaSetDevice(c.device));
-  {  // device-wait timeout of the flag spins (ptx::Spin), COMET_SPIN_TIMEOUT_MS
-    const unsigned long long ms = static_cast<unsigned long long>(std::max(1, env_int("COMET_SPIN_TIMEOUT_MS", 30000)));
-    CK(set_spin_timeout_index(ms * 1000000ull));
-    CK(set_spin_timeout_layers(ms * 1000000ull));
-  }
+  std::copy(kOptDefaults, kOptDefaults + COMET_OPT_COUNT, x->opt);
+  if (int rc = apply_spin_timeout(x)) { delete x; return rc; }
+  // per device: the dynamic shared-memory opt-in of the index kernel
+  CK(cudaFuncSetAttribute(index_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIndexSmem));
   int32_t info[4];
   if (int rc = comet_device_info(c.device, info)) { delete x; return rc; }
   x->n_sm = info[0];
@@ -542,11 +606,6 @@ int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile
   const int chunks = (M + kIndexThreads * ix.tpt - 1) / (kIndexThreads * ix.tpt);
   if (chunks > kIndexMaxChunks) return fail(COMET_EINVAL, "M=%d too large for the index build", M);
   const int grid = std::min(x->n_sm, std::max(32, x->E_r * chunks));
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(index_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIndexSmem));
-    attr_set = true;
-  }
   // global histogram + transfer matrix accumulate by atomics: zero both (adjacent)
   const size_t zbytes = reinterpret_cast<char*>(x->ix.transfer + c.world * c.world) - reinterpret_cast<char*>(x->ix.counts);
   if (flags & kIndexRefLists) CK(cudaMemsetAsync(x->ix.counts, 0, zbytes, static_cast<cudaStream_t>(stream)));
@@ -647,7 +706,11 @@ static int get_weight_map(comet_ctx* x, MapCache& mc, const void* w, uint64_t ro
 static LayerArgs base_args(comet_ctx* x) {
   const auto& c = x->cfg;
   LayerArgs a{};
+#ifdef COMET_TIMING_EXPERIMENTS
+  // timing-experiment bits (layers.cuh LayerArgs::debug): a separate build
+  // only, never the shipped library -- they skip work and give wrong results
   if (const char* d = getenv("COMET_DEBUG")) a.debug = atoi(d);
+#endif
   a.rank = c.rank;
   a.world = c.world;
   a.tp = c.tp;
@@ -683,7 +746,7 @@ static LayerArgs base_args(comet_ctx* x) {
   a.nb_done = x->counters;
   a.nb_sent = x->counters + x->nb1;
   a.mloc_cap = x->mloc_cap;
-  a.ksplit_max = std::max(0, std::min(8, env_int("COMET_KSPLIT", 8)));  // measured: EP=8 M=1K-4K 10-20% faster
+  a.ksplit_max = std::max(0, std::min(8, x->opt[COMET_OPT_KSPLIT_MAX]));  // measured: EP=8 M=1K-4K 10-20% faster
   a.timeline = x->timeline;
   a.timeline_cap = x->timeline_cap;
   return a;
@@ -691,7 +754,7 @@ static LayerArgs base_args(comet_ctx* x) {
 
 static int layer_grid(comet_ctx* x) {
   int grid = std::min(x->n_sm, 2 * x->max_clusters);
-  if (const char* e = getenv("COMET_GRID")) grid = std::min(grid, atoi(e));
+  if (x->opt[COMET_OPT_GRID] > 0) grid = std::min(grid, x->opt[COMET_OPT_GRID]);
   return grid & ~1;
 }
 
@@ -714,7 +777,7 @@ static int launch_kernel(comet_ctx* x, KernelArgs& f, const CUtensorMap& a0, con
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = pdl_on(2) ? 2 : 1;
+  lc.numAttrs = (x->opt[COMET_OPT_PDL] & 2) ? 2 : 1;
   CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, a0, b0, a1, b1, x->tm_Hs, x->tm_ys, f));
   return COMET_OK;
 }
@@ -742,8 +805,9 @@ static int layer0_args(comet_ctx* x, const void* w0t, int activation, int n_comm
   a.order_group = group;
   a.raster = 0;
   a.activation = activation;
-  a.split_tail = env_int("COMET_SPLIT", 1) != 0;
-  a.chunk_rows = std::max(1, std::min(32, env_int("COMET_CHUNK", 32)));
+  a.split_tail = x->opt[COMET_OPT_SPLIT_TAIL0] != 0;
+  a.sequential = x->opt[COMET_OPT_SEQUENTIAL] != 0;
+  a.chunk_rows = std::max(1, std::min(32, x->opt[COMET_OPT_CHUNK_ROWS]));
   a.dedup = 0;
   a.claim_of_tile = x->ix.claim_of_tile;
   a.pairs = x->ix.pairs0;
@@ -777,12 +841,12 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   a.combine_w = combine_w;
   a.y_local = static_cast<__nv_bfloat16*>(y_local);
   // Fused combine (world > 1 always; world 1 when no combine CTAs are asked
-  // for and COMET_FUSE1=1): the epilogue of each token's last hosted row
+  // for and COMET_OPT_FUSE1 is set): the epilogue of each token's last hosted row
   // folds the earlier rows in and writes / pushes the result, so layer1 runs
   // without communication CTAs.  Otherwise combine CTAs (n_comm > 0) or the
   // local combine kernel reduce yrows.  At world 1 the fold's tile waits cost
   // what the local combine kernel saves (A/B in DESIGN.md), so it is opt-in.
-  a.fuse_combine = c.world > 1 || (n_comm == 0 && env_int("COMET_FUSE1", 0) != 0);
+  a.fuse_combine = c.world > 1 || (n_comm == 0 && x->opt[COMET_OPT_FUSE1] != 0);
   a.tile_done = x->tile_done;
   if (c.world > 1 || !alone) n_comm = 0;  // combine CTAs only in a layer1-alone launch at world 1
   const int grid = layer_grid(x);
@@ -796,10 +860,10 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   // EP=8) end layer1 in 256-column halves over 3/4 of the pairs, so the
   // folder epilogues split over twice the CTAs (QW EP=8 0.42 -> 0.40 ms;
   // MX: halves only cost, 0.44 -> 0.47 ms at EP=8 -- off).
-  const int split_env = env_int("COMET_SPLIT1", -1);
-  a.split_units = split_env >= 0 ? split_env
+  const int split1 = x->opt[COMET_OPT_SPLIT1];
+  a.split_units = split1 >= 0 ? split1
                   : (a.fuse_combine && c.topk >= 4 && x->E_r >= 4) ? 3 * (layer_grid(x) / 2) / 4
-                  : env_int("COMET_SPLIT1_AUTO", 1) ? -1 : 0;  // -1: sched.cuh picks by the round count
+                  : -1;  // -1: sched.cuh picks by the round count
   *out = a;
   return COMET_OK;
 }
@@ -809,7 +873,7 @@ static int local_combine(comet_ctx* x, const LayerArgs& a, const float* combine_
   if (a.n_compute < layer_grid(x) || a.fuse_combine) return COMET_OK;  // combine CTAs / epilogue did it
   const int t0 = token_start_of(c.rank, x->M, c.world);
   const int n_tok = token_stop_of(c.rank, x->M, c.world) - t0;
-  CK(launch_pdl(4, combine_local_kernel, dim3(x->n_sm * 8), dim3(256), 0, st, (const int32_t*)x->ix.tok_pos, combine_w,
+  CK(launch_pdl(x->opt[COMET_OPT_PDL], 4, combine_local_kernel, dim3(x->n_sm * 8), dim3(256), 0, st, (const int32_t*)x->ix.tok_pos, combine_w,
                 (const __nv_bfloat16*)x->yrows, static_cast<__nv_bfloat16*>(y_local), t0, n_tok, c.topk, c.N));
   return COMET_OK;
 }
@@ -817,7 +881,7 @@ static int local_combine(comet_ctx* x, const LayerArgs& a, const float* combine_
 static int dispatch_local(comet_ctx* x, cudaStream_t st) {
   const auto& c = x->cfg;
   // HBM-local rows first (whole GPU, bandwidth-bound); dispatch CTAs pull only remote rows.
-  CK(launch_pdl(1, dispatch_local_kernel, dim3(x->n_sm * 4), dim3(256), 0, st, (const int32_t*)x->ix.gather_row,
+  CK(launch_pdl(x->opt[COMET_OPT_PDL], 1, dispatch_local_kernel, dim3(x->n_sm * 4), dim3(256), 0, st, (const int32_t*)x->ix.gather_row,
                 (const int32_t*)x->ix.meta, (const __nv_bfloat16*)x->xs, x->xg, c.N, x->M, c.world, c.rank));
   return COMET_OK;
 }
@@ -860,18 +924,17 @@ int comet_layers(comet_ctx* x, const void* w0t, const void* w1t, const float* co
   // keeps the expert-ascending table (a token's earlier hosted rows must sit
   // in earlier units of the same columns).
   f.l[1].raster = 2;
-  f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
+  f.l[1].order_group2 = group1(x, f.l[0].order_group);
   // layer0's last partial round in halves too: the layer1 units of its pairs
   // wait for it (critical path = last layer0 unit + one layer1 unit)
-  f.l[0].split_tail = env_int("COMET_SPLIT0", 1) != 0;
   if (!f.l[1].fuse_combine || x->E_r == 1 || x->cfg.topk == 1) f.l[1].pairs = x->ix.pairs0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // world > 1: the dispatch CTAs place the local rows too (locality-first:
   // they are the first tiles claimed), saving the local-dispatch launch
-  f.l[0].pull_local = x->cfg.world > 1 && env_int("COMET_PULL_LOCAL", 1) != 0;
+  f.l[0].pull_local = x->cfg.world > 1 && x->opt[COMET_OPT_PULL_LOCAL] != 0;
   // per-token dedup of the NVLink pulls (dispatch_rows_dedup; one read per
   // (token, rank), fanned out to the token's hosted rows)
-  f.l[0].dedup = f.l[0].pull_local && x->cfg.topk <= 8 && env_int("COMET_DEDUP", 0) != 0;
+  f.l[0].dedup = f.l[0].pull_local && x->cfg.topk <= 8 && dedup_on(x);
   if (!f.l[0].pull_local)
     if (int rc = dispatch_local(x, st)) return rc;
   if (int rc = launch_kernel(x, f, x->tm_xg, x->w0c.map, x->tm_H, x->w1c.map, st)) return rc;
@@ -916,7 +979,7 @@ int comet_combine_finish(comet_ctx* x, void* y_local, void* stream) {
   const int n_own = token_stop_of(c.rank, x->M, c.world) - token_start_of(c.rank, x->M, c.world);
   const int items = n_own * ((c.N / 8 + 127) / 128);  // one warp per (token, 1024-column segment)
   const int blocks = std::max(1, std::min(x->n_sm * 8, (items + 7) / 8));
-  CK(launch_pdl(4, combine_finish_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), a,
+  CK(launch_pdl(x->opt[COMET_OPT_PDL], 4, combine_finish_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), a,
                 (const __nv_bfloat16*)x->cb, (const uint32_t*)x->cb_flag, (const int32_t*)x->ix.experts));
   CK(cudaGetLastError());
   return COMET_OK;
@@ -930,15 +993,15 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
   // world > 1 with fold chains (several hosted experts per token): order the
   // layer1 pairs by fold level (COMET_FOLD_ORDER=0 keeps expert order)
   const bool fold_order = x->cfg.world > 1 && x->E_r > 1 && x->E_r <= 64 && x->cfg.topk > 1 &&
-                          env_int("COMET_FOLD_ORDER", 1) != 0;
+                          x->opt[COMET_OPT_FOLD_ORDER] != 0;
   const int flags = (x->cfg.world == 1 && n_comm1 > 0 ? kIndexCombineList : 0) |
                     (x->cfg.world > 1 ? kIndexSignal : 0) | (fold_order ? kIndexFoldOrder : 0);
   if (int rc = comet_index_build_ex(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), flags,
                                     stream))
     return rc;
   // One launch for both layers (layer1 tiles start as their H rows land),
-  // unless world-1 combine CTAs are asked for or COMET_FUSED=0.
-  const bool fused = env_int("COMET_FUSED", 1) != 0 && !(x->cfg.world == 1 && n_comm1 > 0);
+  // unless world-1 combine CTAs are asked for or COMET_OPT_FUSED is 0.
+  const bool fused = x->opt[COMET_OPT_FUSED] != 0 && !(x->cfg.world == 1 && n_comm1 > 0);
   if (fused) {
     if (int rc = comet_layers(x, w0t, w1t, combine_w, y_local, activation, n_comm0, group0, wave1, stream)) return rc;
   } else {
@@ -1023,11 +1086,11 @@ int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, 
   f.l[0].chunk_tokens = ct;
   f.l[0].split_tail = 0;
   f.l[1].raster = 2;
-  f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
+  f.l[1].order_group2 = group1(x, f.l[0].order_group);
   f.l[1].pairs = x->ix.pairs0;  // (row tile, expert) order
   // the dispatch CTAs reduce finished token chunks (no layer1 unit waits for
   // another); COMET_STREAM_FUSE=1: the epilogue fold (folder claimed last)
-  const bool fold = env_int("COMET_STREAM_FUSE", 0) != 0;
+  const bool fold = x->opt[COMET_OPT_STREAM_FUSE] != 0;
   f.l[0].stream_combine = fold ? 0 : 1;
   f.l[1].fuse_combine = fold ? 1 : 0;
   f.l[1].publish_tiles = 1;
@@ -1085,15 +1148,15 @@ int comet_forward_zerocopy(comet_ctx* x, const void* h_x, const int32_t* h_exper
   // were mostly pulled for the same row tile of the previous experts, so the
   // PCIe bytes per tile are uniform instead of front-loaded (measured slower:
   // 3.7 vs 3.4 ms, consecutive units cycle through the experts' weights)
-  const bool tile_order = env_int("COMET_ZC_ORDER", 0) != 0;
+  const bool tile_order = x->opt[COMET_OPT_ZC_ORDER] != 0;
   const bool fold_order = !tile_order && x->E_r > 1 && x->E_r <= 64 && c.topk > 1 &&
-                          env_int("COMET_FOLD_ORDER", 0) != 0;
+                          x->opt[COMET_OPT_ZC_FOLD_ORDER] != 0;
   if (int rc = comet_index_build_ex(x, x->routing, M, 128, c.N >= 512 ? 128 : std::max(1, c.N / 4),
                                     (fold_order ? kIndexFoldOrder : 0) | (tile_order ? kIndexStream : 0), stream))
     return rc;
   // n_dl of the dispatch CTAs download the output afterwards (the fused
   // combine writes a device copy); n_dl = 0: the epilogues write h_y directly
-  const int n_dl = std::min(n_comm0, std::max(0, env_int("COMET_ZC_DL", 8))) & ~1;
+  const int n_dl = std::min(n_comm0, std::max(0, x->opt[COMET_OPT_ZC_DOWNLOAD])) & ~1;
   if (n_dl > 0 && !x->y_stream) CK(cudaMalloc(&x->y_stream, (size_t)c.m_cap * c.N * 2));
   KernelArgs f{};
   if (int rc = layer0_args(x, w0t, activation, 0, group0, &f.l[0])) return rc;
@@ -1104,21 +1167,20 @@ int comet_forward_zerocopy(comet_ctx* x, const void* h_x, const int32_t* h_exper
   f.y_host = static_cast<__nv_bfloat16*>(h_y);
   f.l[0].n_compute = layer_grid(x) - n_comm0;
   f.l[0].pull_local = 1;
-  f.l[0].dedup = env_int("COMET_ZC_DEDUP", 1) != 0;
+  f.l[0].dedup = x->opt[COMET_OPT_ZC_DEDUP] != 0;
   f.l[0].host_src = static_cast<const __nv_bfloat16*>(h_x);
-  f.l[0].split_tail = env_int("COMET_SPLIT0", 1) != 0;
   f.l[1].raster = 2;
-  f.l[1].order_group2 = env_int("COMET_G1", f.l[0].order_group);
+  f.l[1].order_group2 = group1(x, f.l[0].order_group);
   f.l[1].fuse_combine = 1;
   if (x->E_r == 1 || c.topk == 1 || tile_order) f.l[1].pairs = x->ix.pairs0;
-  // Interleave the layers (COMET_ZC_ILV groups of lag, default 1 with the
+  // Interleave the layers (COMET_OPT_ZC_INTERLEAVE groups of lag, default 1 with the
   // 16-pair groups the host layer passes; 0 = layer1 after all
   // of layer0): the dispatch is PCIe-paced, so layer0 alone leaves the
   // tensor cores waiting; layer1 groups of finished pairs fill the gaps and
   // start the host writes early.  Needs one pair order for both layers: at
   // world 1 the claim order is expert-ascending like pairs1 (no fold-level
   // order), and no split tails / split-K.
-  f.interleave = fold_order ? 0 : env_int("COMET_ZC_ILV", 1);
+  f.interleave = fold_order ? 0 : std::max(0, x->opt[COMET_OPT_ZC_INTERLEAVE]);
   if (f.interleave > 0) {
     f.l[1].pairs = x->ix.pairs0;
     f.l[1].order_group2 = f.l[0].order_group;

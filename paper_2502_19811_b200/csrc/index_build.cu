@@ -618,3 +618,6 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
 cudaError_t set_spin_timeout_index(unsigned long long ns) {
   return cudaMemcpyToSymbol(comet::ptx::g_spin_timeout_ns, &ns, sizeof(ns));
 }
+cudaError_t set_abort_flag_index(const volatile uint32_t* p) {
+  return cudaMemcpyToSymbol(comet::ptx::g_abort_flag, &p, sizeof(p));
+}

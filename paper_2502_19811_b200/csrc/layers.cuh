@@ -7,6 +7,14 @@
 
 #include "index.cuh"
 
+// Timing-experiment switches (LayerArgs::debug) exist only in a build with
+// -DCOMET_TIMING_EXPERIMENTS; the shipped library folds them to false.
+#ifdef COMET_TIMING_EXPERIMENTS
+#define COMET_DBG(v, bits) ((((v) & (bits)) != 0))
+#else
+#define COMET_DBG(v, bits) false
+#endif
+
 namespace comet {
 
 enum TimelineRole : int { kRoleLoad = 0, kRoleMma = 1, kRoleTmemWait = 2, kRoleEpilogue = 3, kRoleComm = 4, kRoles = 5 };
@@ -36,10 +44,12 @@ struct LayerArgs {
   float* part;            // split-K fp32 partials [tiles*NB][S][128][512] (<= pairs*2 CTA tiles)
   uint32_t* split_cnt;    // [tiles*NB] slices landed (reset by the finisher)
   uint32_t epoch;
-  int debug;              // COMET_DEBUG bits (timing experiments, wrong results unless noted):
-                          // 1: comm CTAs idle; 8: no MMA; 16: no loads; 32: sequential (GEMMs start
-                          // after the whole dispatch; correct, the cli baseline); 64/128: no stores /
-                          // no drain; 16384: st.global epilogue instead of TMA stores (correct)
+  int debug;              // timing-experiment bits, compiled in only with -DCOMET_TIMING_EXPERIMENTS
+                          // (COMET_DBG; wrong results unless noted): 1: comm CTAs idle; 4: spin
+                          // waits; 8: no MMA; 16: no loads; 64/128: no stores / no drain; 16384:
+                          // st.global epilogue instead of TMA stores (correct)
+  int sequential;         // layer0: GEMMs start after the WHOLE dispatch (COMET_OPT_SEQUENTIAL; the
+                          // no-overlap baseline of the cli, correct results)
 
   // index (device)
   const int32_t* meta;

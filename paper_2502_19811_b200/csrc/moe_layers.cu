@@ -194,8 +194,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = blockIdx.x & 1;  // rank in the 2-CTA cluster
   const bool leader = cta == 0;
-  const int dbg = f.l[f.mode == 1 ? 1 : 0].debug;
-  const bool spin = (dbg & 4) != 0;
+  const bool spin = COMET_DBG(f.l[f.mode == 1 ? 1 : 0].debug, 4);
   auto wait = [spin](uint64_t* bar, uint32_t parity) {
     if (spin) ptx::mbar_wait_spin(bar, parity);
     else ptx::mbar_wait(bar, parity);
@@ -294,7 +293,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
       const int brow = pr.x * p.b_rows + w.nb * kBlockN + 128 * static_cast<int>(cta) + (w.half > 0 ? kHalfN : 0);
-      if (lane == 0 && w.layer == 0 && (p.debug & 32) && !seq_done && !(p.debug & 1)) {
+      if (lane == 0 && w.layer == 0 && p.sequential && !seq_done) {
         // "sequential" mode (no overlap, the cli's baseline): the first GEMM
         // waits for the WHOLE dispatch, like an all-to-all before GroupGEMM
         for (int q = 0; q < 2 * P; ++q)
@@ -305,7 +304,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       }
       if (lane == 0) {
         const bool pulled = p.pull_local ? pr.z > kTileRows * static_cast<int>(cta) : ((pr.w >> cta) & 1);
-        if (w.layer == 0 && pulled && !(p.debug & 1)) {
+        if (w.layer == 0 && pulled && !COMET_DBG(p.debug, 1)) {
           // this CTA's 128 A rows include rows pulled over NVLink by a dispatch CTA
           const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
           { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) sp.pause(32, 3); }
@@ -326,7 +325,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       for (int kb = kb0; kb < kb1; ++kb) {
         wait(empty + stage, phase ^ 1);
         if (kb == kb_req && leader && lane == 0) ptx::mbar_arrive(sreq);  // claim the next unit now
-        if (lane == 0 && (p.debug & 16)) {
+        if (lane == 0 && COMET_DBG(p.debug, 16)) {
           // debug: no data movement, complete the stage by arrivals only
           if (leader) ptx::mbar_arrive(full + stage);
           else ptx::mbar_arrive_cluster(full + stage, 0);
@@ -370,7 +369,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         const uint64_t db0 = ptx::sdesc_kmajor_sw128(sa + kSmemA);
         const uint64_t db1 = ptx::sdesc_kmajor_sw128(sa + kSmemA + kSmemBh);
         // one fixed issuing lane: tcgen05.commit tracks the MMAs of its own thread
-        if (lane == 0 && !(p.debug & 8)) {
+        if (lane == 0 && !COMET_DBG(p.debug, 8)) {
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k)
             ptx::mma_bf16_2sm(tmem_base, da + 2 * k, db0 + 2 * k, kIdesc, (kb != kb0) || (k != 0));
@@ -381,7 +380,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           ptx::tc_fence_after();
         }
         if (lane == 0) {
-          if (!(p.debug & 8) && two) {
+          if (!COMET_DBG(p.debug, 8) && two) {
 #pragma unroll
             for (int k = 0; k < kBlockK / 16; ++k)
               ptx::mma_bf16_2sm(tmem_base + kHalfN, da + 2 * k, db1 + 2 * k, kIdesc, (kb != kb0) || (k != 0));
@@ -473,7 +472,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // coalesced stores
       // contiguous destination rows (H, or yrows without the fused combine):
       // TMA tensor stores; fused-combine units write scattered token rows
-      const bool tma_out = (w.layer == 0 || !p.fuse_combine) && !(p.debug & 16384);
+      const bool tma_out = (w.layer == 0 || !p.fuse_combine) && !COMET_DBG(p.debug, 16384);
       auto process = [&](int s, uint32_t (&v0)[32], uint32_t (&v1)[32]) {
         if (w.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
 #pragma unroll
@@ -565,7 +564,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
 #pragma unroll 1
       for (int s = 0; s < n_chunks; ++s) {
         const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
-        if (p.debug & 128) {  // debug: drain nothing
+        if (COMET_DBG(p.debug, 128)) {  // debug: drain nothing
           if (half_end) {
             ptx::tc_fence_before();
             if (leader) ptx::mbar_arrive(tempty + (s * 64 >= static_cast<int>(kHalfN)));
@@ -604,7 +603,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           }
           continue;
         }
-        if (s * 64 >= cols_left || (p.debug & 64)) continue;
+        if (s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;
         process(s, v0, v1);
       }
       if (tma_out) {  // this warp's tensor stores complete before the unit is counted
@@ -626,7 +625,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           const float4* rows0 = reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + ew * 32 + lane;
 #pragma unroll 1
           for (int s = 0; s < n_chunks; ++s) {
-            if (s * 64 >= cols_left || (p.debug & 64)) continue;
+            if (s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;
             uint32_t v0[32], v1[32];
             float acc[64];
 #pragma unroll
@@ -729,12 +728,12 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
   if (f.mode == 1 && b >= f.l[1].n_compute) {
     // layer1 combine CTA (world 1, comm-CTA combine): reduces to the end
     ptx::pdl_wait();
-    if (!(f.l[1].debug & 1)) comm::combine_reduce(f.l[1], smem);
+    if (!COMET_DBG(f.l[1].debug, 1)) comm::combine_reduce(f.l[1], smem);
     compute = false;
   } else if (f.mode != 1 && b >= f.l[0].n_compute) {
     // layer0 dispatch CTA: pull the remote rows, then join the compute pairs
     ptx::pdl_wait();
-    if (!(f.l[0].debug & 1)) {
+    if (!COMET_DBG(f.l[0].debug, 1)) {
       if (f.l[0].dedup) comm::dispatch_rows_dedup(f.l[0], smem);
       else comm::dispatch_rows(f.l[0], smem);
     }
@@ -930,4 +929,7 @@ __global__ void signal_x_ready_kernel(uint32_t* const* x_ready_peer, int rank, i
 // host: this unit's device-wait timeout (ptx::Spin)
 cudaError_t set_spin_timeout_layers(unsigned long long ns) {
   return cudaMemcpyToSymbol(comet::ptx::g_spin_timeout_ns, &ns, sizeof(ns));
+}
+cudaError_t set_abort_flag_layers(const volatile uint32_t* p) {
+  return cudaMemcpyToSymbol(comet::ptx::g_abort_flag, &p, sizeof(p));
 }

@@ -377,11 +377,14 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
 // instead of hanging the GPU.  The clock is read every 64 polls; the report
 // is out of line (no stack or registers in the callers' hot code).
 // per translation unit (no relocatable device code); set at context creation
-// from COMET_SPIN_TIMEOUT_MS by each unit's set_spin_timeout_* (default 30 s)
-static __device__ unsigned long long g_spin_timeout_ns = 30ull * 1000 * 1000 * 1000;
-__device__ __noinline__ inline void spin_timeout(int site) {
-  printf("comet: device wait timed out (site %d, block %d, thread %d)\n", site, static_cast<int>(blockIdx.x),
-         static_cast<int>(threadIdx.x));
+// from COMET_OPT_SPIN_TIMEOUT_MS by each unit's set_spin_timeout_* (default
+// 10 min), and the host abort word of comet_abort_waits (mapped pinned
+// memory, polled with the clock)
+static __device__ unsigned long long g_spin_timeout_ns = 600ull * 1000 * 1000 * 1000;
+static __device__ const volatile uint32_t* g_abort_flag = nullptr;
+__device__ __noinline__ inline void spin_timeout(int site, bool aborted) {
+  printf("comet: device wait %s (site %d, block %d, thread %d)\n", aborted ? "aborted by the host" : "timed out",
+         site, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));
   __trap();
 }
 struct Spin {
@@ -394,8 +397,9 @@ struct Spin {
     if (t0 == 0) {
       t0 = t;
     } else if (t - t0 > g_spin_timeout_ns) {
-      spin_timeout(site);
+      spin_timeout(site, false);
     }
+    if (g_abort_flag != nullptr && *g_abort_flag != 0u) spin_timeout(site, true);
   }
 };
 

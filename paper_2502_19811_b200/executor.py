@@ -146,19 +146,56 @@ class LayerKnobs:
     """Kernel knobs.  n_comm0/n_comm1 are the paper's communication-block
     counts n_c (simulator.py:45-65), chosen by ``assigner.select_split`` from
     measured timings; group0 / wave1 set the layer0 L2 grouping and the
-    layer1 column-wave width."""
+    layer1 column-wave width.  ``zc_*`` / ``stream_n_comm`` size the
+    single-GPU host-buffer forwards.  The remaining fields are the context
+    options of include/comet_b200.h (COMET_OPT_*, ``_lib.OPTIONS``): None
+    keeps the library's measured default.  Nothing is read from the
+    environment."""
 
     n_comm0: int = 64
     n_comm1: int = 0
     group0: int = 4
     wave1: int = 4
+    zc_n_comm: int = 16
+    zc_group0: int = 16
+    stream_n_comm: int = 16
+    fused: Optional[bool] = None
+    ksplit_max: Optional[int] = None
+    split_tail0: Optional[bool] = None
+    split1: Optional[int] = None
+    dedup: Optional[int] = None
+    pull_local: Optional[bool] = None
+    fold_order: Optional[bool] = None
+    group1: Optional[int] = None
+    chunk_rows: Optional[int] = None
+    pdl: Optional[int] = None
+    grid: Optional[int] = None
+    fuse1: Optional[bool] = None
+    spin_timeout_ms: Optional[int] = None
+    zc_dedup: Optional[bool] = None
+    zc_interleave: Optional[int] = None
+    zc_download: Optional[int] = None
+    zc_order: Optional[bool] = None
+    zc_fold_order: Optional[bool] = None
+    stream_fuse: Optional[bool] = None
+    sequential: Optional[bool] = None
 
     @classmethod
-    def for_world(cls, world: int) -> "LayerKnobs":
-        """Measured defaults (bench.py / tools/gpu_runs/gpu_run105-106.sh): 8
-        dispatch CTAs per rank of the group (max 64); 8-pair layer0 groups at
-        EP=1 and EP>=8, 4-pair groups at EP=2/4."""
-        return cls(n_comm0=min(64, 8 * max(1, world)), group0=8 if world == 1 or world >= 8 else 4)
+    def for_world(cls, world: int, **options) -> "LayerKnobs":
+        """Measured defaults (bench.py): 8 dispatch CTAs per rank
+        of the group (max 64); 8-pair layer0 groups at EP=1 and EP>=8, 4-pair
+        groups at EP=2/4."""
+        return cls(n_comm0=min(64, 8 * max(1, world)), group0=8 if world == 1 or world >= 8 else 4, **options)
+
+    def options(self) -> Dict[str, Optional[int]]:
+        """The COMET_OPT_* values (None = library default)."""
+        return {name: (None if getattr(self, name) is None else int(getattr(self, name))) for name in _lib.OPTIONS}
+
+    def is_fused(self, world: int) -> bool:
+        """Both layers in one persistent launch (comet_layers) -- the default,
+        as in comet_forward -- unless world-1 combine CTAs are asked for or
+        ``fused`` is False."""
+        return self.fused is not False and not (world == 1 and self.n_comm1 > 0)
 
 
 class MoELayer:
@@ -183,9 +220,25 @@ class MoELayer:
         self.torch = self.ctx.torch
         self.weights = weights
         self.act = activation_code(activation)
+        self._applied: Optional[Dict[str, Optional[int]]] = None
         self.knobs = knobs or LayerKnobs.for_world(parallel.world_size)
         self.device = device
         self._xbuf = self.ctx.token_buffer()
+
+    @property
+    def knobs(self) -> LayerKnobs:
+        return self._knobs
+
+    @knobs.setter
+    def knobs(self, knobs: LayerKnobs) -> None:
+        """Install knobs: the COMET_OPT_* fields go to the native context."""
+        opts = knobs.options()
+        if opts != self._applied:
+            for name, value in opts.items():
+                if self._applied is None or self._applied.get(name) != value:
+                    self.ctx.set_option(name, value)
+            self._applied = opts
+        self._knobs = knobs
 
     def token_range(self, M: int):
         w = self.parallel.world_size
@@ -245,68 +298,72 @@ class MoELayer:
         self.run(ex.contiguous(), M, y, cw)
         return y if self.n_pad == self.model.N else y[:, :self.model.N]
 
-    def forward_host(self, x_host, experts_host, combine_w=None, out=None, chunks: Optional[int] = None):
-        """End-to-end form on HOST buffers (pinned for overlap): H2D of the
-        tokens and router output, the forward, D2H of the result into ``out``
-        (allocated pinned when None); asynchronous on the current stream like
+    def forward_host(self, x_host, experts_host, combine_w=None, out=None, chunks=None,
+                     mode: Optional[str] = None):
+        """End-to-end form on HOST buffers (pinned for overlap): tokens and
+        router output in, the result into ``out`` (bf16 [M_r, N], allocated
+        pinned when None); asynchronous on the current stream like
         ``forward`` (synchronise it before reading ``out``).
 
-        Single GPU, default (COMET_E2E=zerocopy; pinned ``x_host``/``out``):
-        ONE launch with the host as the token-owning peer
-        (``comet_forward_zerocopy``): dispatch CTAs read each token row once
-        from pinned host memory over PCIe in the compute claim order and the
-        fused combine writes output rows straight to ``out``.
+        ``mode`` (single GPU; default "zerocopy" when ``out`` is pinned,
+        contiguous bf16 and N % 512 == 0, else "chunks"):
 
-        Single GPU, COMET_E2E=stream: ONE streamed launch
-        (``comet_forward_host``): the token upload runs in 1024-token chunks
-        whose landing the dispatch CTAs wait for, and the download of each
-        chunk starts as soon as the fused combine finished its rows.  Correct
-        (tests) but not yet faster: at world 1 the fused combine's folder
-        waits for its sibling row's unit, which runs concurrently (layer1
-        units 150 -> 220 us; 4.2 vs 4.1 ms, tools/stream_probe.py).  Default:
-        the M tokens run as
-        consecutive forwards over token chunks with the H2D of chunk c+1 and
-        the D2H of chunk c-1 on two copy streams under the forward of chunk
-        c.  Only the first chunk's upload and the last chunk's download stay
-        exposed (COMET_E2E=chunks or an explicit ``chunks``; default 3 equal
-        chunks for M >= 6144; ``chunks`` = an int for equal chunks or a list
-        of sizes).  Multi-GPU ranks copy, run, copy."""
+        * "zerocopy": ONE launch with the host as the token-owning peer
+          (``comet_forward_zerocopy``): dispatch CTAs read each token row once
+          from pinned host memory over PCIe in the compute claim order and the
+          fused combine writes output rows to ``out``.  A token tensor that is
+          not pinned contiguous bf16 is first converted into a pinned staging
+          buffer owned by the layer (the kernel reads it asynchronously).
+        * "stream": ONE streamed launch (``comet_forward_host``): the token
+          upload runs in 1024-token chunks whose landing the dispatch CTAs
+          wait for, the download of each chunk starts as soon as the fused
+          combine finished its rows.  Correct (tests) but slower than
+          zerocopy.
+        * "chunks": consecutive forwards over token chunks with the H2D of
+          chunk c+1 and the D2H of chunk c-1 on two copy streams under the
+          forward of chunk c (``chunks`` = an int for equal chunks or a list
+          of sizes; default 3 equal chunks for M >= 6144).
+
+        Multi-GPU ranks copy, run, copy."""
         torch = self.torch
         M = int(experts_host.shape[0])
         N = self.model.N
         lo_r, hi_r = self.token_range(M)
         if out is None:
             out = torch.empty(hi_r - lo_r, N, dtype=torch.bfloat16, pin_memory=True)
+        if tuple(out.shape) != (hi_r - lo_r, N):
+            raise ConfigurationError(f"out must be [{hi_r - lo_r}, {N}], got {tuple(out.shape)}")
         world = self.parallel.world_size
-        import os
-        e2e_mode = os.environ.get("COMET_E2E", "zerocopy")
-        if (world == 1 and chunks is None and e2e_mode == "zerocopy" and self.n_pad == N
-                and N % 512 == 0 and self.model.topk <= 8 and x_host.is_pinned() and out.is_pinned()
-                and out.is_contiguous()):
+        out_direct = out.dtype == torch.bfloat16 and out.is_contiguous() and out.is_pinned()
+        if mode is None:
+            mode = "zerocopy" if chunks is None else "chunks"
+        if mode not in ("zerocopy", "stream", "chunks"):
+            raise ConfigurationError(f"forward_host mode {mode!r}: choose zerocopy, stream or chunks")
+        single = world == 1 and self.n_pad == N and out_direct
+        k = self.knobs
+        if single and mode == "zerocopy" and N % 512 == 0 and self.model.topk <= 8:
             # one launch, the host as the token-owning peer (comet_forward_zerocopy)
             ex = experts_host if experts_host.dtype == torch.int32 else experts_host.to(torch.int32)
             cw = None if combine_w is None else combine_w.float().contiguous()
-            xb = x_host if x_host.dtype == torch.bfloat16 else x_host.to(torch.bfloat16)
-            k = self.knobs
+            xb = self._pinned_tokens(x_host, M)
             # 16-pair groups, layer1 one group behind (PCIe-paced dispatch: a
             # group spans two experts' tiles, whose token rows land together
             # with the per-token dedup; 3.50 -> 3.40 ms vs 8-pair groups, lag 3)
-            self.ctx.forward_zerocopy(xb.contiguous(), ex.contiguous(), cw, out, M, self.weights.w0t,
-                                      self.weights.w1t, self.act, n_comm0=int(os.environ.get("COMET_ZC_NC", 16)),
-                                      group0=int(os.environ.get("COMET_ZC_G0", 16)), wave1=k.wave1)
+            self.ctx.forward_zerocopy(xb, ex.contiguous(), cw, out, M, self.weights.w0t, self.weights.w1t, self.act,
+                                      n_comm0=k.zc_n_comm, group0=k.zc_group0, wave1=k.wave1)
+            self._note_host_reader()
             return out
-        if (world == 1 and chunks is None and e2e_mode == "stream"
-                and self.n_pad == N and x_host.is_pinned() and out.is_pinned() and out.is_contiguous()):
+        if single and mode == "stream":
             # one launch streaming the upload / download (comet_forward_host)
             ex = experts_host if experts_host.dtype == torch.int32 else experts_host.to(torch.int32)
             cw = None if combine_w is None else combine_w.float().contiguous()
-            xb = x_host if x_host.dtype == torch.bfloat16 else x_host.to(torch.bfloat16)
-            k = self.knobs
+            xb = self._pinned_tokens(x_host, M)
             # the dispatch CTAs also reduce the combine (they do not join the
             # GEMMs here): a small count
-            self.ctx.forward_host(xb.contiguous(), ex.contiguous(), cw, out, M, self.weights.w0t, self.weights.w1t,
-                                  self.act, n_comm0=int(os.environ.get("COMET_STREAM_NC", 16)), group0=k.group0,
+            self.ctx.forward_host(xb, ex.contiguous(), cw, out, M, self.weights.w0t, self.weights.w1t,
+                                  self.act, n_comm0=k.stream_n_comm, group0=k.group0,
                                   wave1=k.wave1, chunks=max(1, min(64, M // 1024)))
+            self._note_host_reader()
             return out
         sizes = _chunk_sizes(M, chunks)
         if world > 1 or len(sizes) <= 1:
@@ -364,6 +421,30 @@ class MoELayer:
         comp.wait_event(last)
         return out
 
+    def _pinned_tokens(self, x_host, M: int):
+        """``x_host`` as pinned contiguous bf16 host memory that stays alive
+        while the kernel reads it: the caller's tensor when it already is,
+        else a staging buffer owned by the layer (reused once the previous
+        host-reading launch is done)."""
+        torch = self.torch
+        if (x_host.dtype == torch.bfloat16 and x_host.is_contiguous() and x_host.is_pinned()
+                and x_host.device.type == "cpu"):
+            return x_host
+        st = getattr(self, "_x_stage", None)
+        if st is None or st.shape[0] < M or st.shape[1] != x_host.shape[1]:
+            st = torch.empty(max(M, 1), x_host.shape[1], dtype=torch.bfloat16, pin_memory=True)
+            self._x_stage = st
+        ev = getattr(self, "_host_reader", None)
+        if ev is not None:
+            ev.synchronize()  # the previous launch has finished reading the staging buffer
+        st[:M].copy_(x_host.to("cpu"))
+        return st[:M]
+
+    def _note_host_reader(self) -> None:
+        ev = self.torch.cuda.Event()
+        ev.record(self.torch.cuda.current_stream(self.device))
+        self._host_reader = ev
+
     def close(self) -> None:
         self.ctx.close()
 
@@ -399,12 +480,31 @@ def _check_input(x, routing: RoutingTable):
             f"input must be shaped (M={routing.workload.M}, N={routing.model.N}), got {shape}")
 
 
-def _rank_weights(weights: ExpertWeights, model: ModelConfig, parallel: ParallelSpec) -> List[RankWeights]:
+def invalidate_weight_cache(weights: Optional[ExpertWeights] = None) -> None:
+    """Drop the prepared device copies of ``weights`` (all when None)."""
+    if weights is None:
+        _weight_cache.clear()
+    else:
+        _weight_cache.pop(weights, None)
+
+
+def _rank_weights(weights, model: ModelConfig, parallel: ParallelSpec) -> List[RankWeights]:
+    """Per-rank bf16 device copies.  ``weights`` is an ``ExpertWeights``
+    (cached per instance: its arrays are made read-only while cached, so an
+    in-place edit raises instead of silently using stale copies; call
+    ``invalidate_weight_cache`` after replacing them) or a ``(w0, w1)`` pair
+    of torch tensors, e.g. on the GPU for full-size shapes (not cached)."""
+    if isinstance(weights, tuple):
+        w0, w1 = weights
+        return [RankWeights.from_full(w0, w1, model, parallel, r) for r in range(parallel.world_size)]
     key = (model, parallel)
     per = _weight_cache.get(weights)
     if per is None:
         per = {}
         _weight_cache[weights] = per
+        for arr in (weights.w0, weights.w1):
+            if isinstance(arr, np.ndarray):
+                arr.flags.writeable = False
     if key not in per:
         per[key] = [RankWeights.from_full(weights.w0, weights.w1, model, parallel, r)
                     for r in range(parallel.world_size)]
@@ -412,28 +512,39 @@ def _rank_weights(weights: ExpertWeights, model: ModelConfig, parallel: Parallel
 
 
 def _layers(model: ModelConfig, parallel: ParallelSpec, m_cap: int, rw: List[RankWeights], act: int):
-    key = (model, parallel, m_cap)
-    layers = _group_cache.get(key)
-    if layers is None:
-        if len(_group_cache) > 8:
-            for group in _group_cache.values():
-                for layer in group:
-                    layer.close()
-            _group_cache.clear()
-        layers = [MoELayer(model, parallel, r, m_cap, rw[r]) for r in range(parallel.world_size)]
+    """Emulated rank layers for (model, parallel), sized for >= m_cap tokens
+    (capacity rounded up to a power of two so varying M reuses the group;
+    at most 4 groups are kept, least recently used evicted and freed)."""
+    cap = 1 << max(0, int(m_cap - 1).bit_length())
+    key = None
+    for k in _group_cache:
+        if k[0] == model and k[1] == parallel and k[2] >= m_cap:
+            key = k
+            break
+    if key is None:
+        while len(_group_cache) >= 4:
+            old = next(iter(_group_cache))
+            for layer in _group_cache.pop(old):
+                layer.close()
+        key = (model, parallel, cap)
+        layers = [MoELayer(model, parallel, r, cap, rw[r]) for r in range(parallel.world_size)]
         if parallel.world_size > 1:
             _lib.Context.link_local([layer.ctx for layer in layers])
         _group_cache[key] = layers
+    layers = _group_cache.pop(key)
+    _group_cache[key] = layers  # most recently used last
     for r, layer in enumerate(layers):
         layer.weights = rw[r]
         layer.act = act
     return layers
 
 
-def run_emulated(x, weights: ExpertWeights, routing: RoutingTable, parallel: ParallelSpec,
+def run_emulated(x, weights, routing: RoutingTable, parallel: ParallelSpec,
                  activation: Activation = None, combine_weights=None, knobs: Optional[LayerKnobs] = None):
     """Execute the layer with every rank of ``parallel`` on this GPU (shared
-    by the three reference entry points).  Returns a torch fp32 [M, N]."""
+    by the three reference entry points).  ``weights``: ``ExpertWeights`` or
+    a ``(w0 [E,N,K], w1 [E,K,N])`` pair of torch tensors.  Returns a torch
+    fp32 [M, N]."""
     torch = _lib.require_device()
     model = routing.model
     act = activation_code(activation)
@@ -452,8 +563,7 @@ def run_emulated(x, weights: ExpertWeights, routing: RoutingTable, parallel: Par
     if M == 0:
         return out[:, :model.N].float()
     for layer in layers:
-        if knobs is not None:
-            layer.knobs = knobs
+        layer.knobs = knobs if knobs is not None else LayerKnobs.for_world(parallel.world_size)
         lo, hi = layer.token_range(M)
         layer.place_tokens(xt[lo:hi], M)
     _phase_forward(layers, ex, M, [out[slice(*layer.token_range(M))] for layer in layers], cw)
@@ -467,14 +577,6 @@ def index_flags(world: int, n_comm1: int) -> int:
     return (2 if world == 1 and n_comm1 > 0 else 0) | (4 if world > 1 else 0)
 
 
-def fused_launch(world: int, n_comm1: int) -> bool:
-    """Both layers in one persistent launch (comet_layers) -- the default,
-    as in comet_forward -- unless world-1 combine CTAs are asked for or
-    COMET_FUSED=0."""
-    import os
-    return os.environ.get("COMET_FUSED", "1") != "0" and not (world == 1 and n_comm1 > 0)
-
-
 def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
     """Enqueue a forward of every emulated rank, phase by phase, on one
     stream: each in-kernel wait is on work enqueued before it, so ranks that
@@ -485,7 +587,7 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
         # hot path: the kernels' tables only (+ the combine list for world-1
         # combine CTAs); world > 1: the build also publishes the x_ready epoch
         layer.ctx.index_build(ex, M, stream=stream, flags=index_flags(world, layer.n_comm1()))
-    if fused_launch(world, layers[0].n_comm1()):
+    if layers[0].knobs.is_fused(world):
         for layer, y in zip(layers, outs):
             k = layer.knobs
             layer.ctx.layers(layer.weights.w0t, layer.weights.w1t, cw, y, layer.act,
@@ -563,6 +665,32 @@ def execute_tp_sharded(x, weights: ExpertWeights, routing: RoutingTable, tp: int
 _RANK_LAYERS: Dict[tuple, "MoELayer"] = {}
 
 
+def _rank_layer(model: ModelConfig, par: ParallelSpec, M: int, w_local: RankWeights, activation: Activation,
+                knobs: Optional[LayerKnobs]) -> "MoELayer":
+    """This rank's cached layer for (model, parallel, activation), with a
+    token capacity >= M (rounded up to a power of two, so varying batch sizes
+    reuse it); the weights are passed per call.  Creating one is collective
+    (``distributed.init_layer``); every rank takes the same branch because the
+    decision depends only on arguments all ranks share.  At most two layers
+    are kept (the older one is closed)."""
+    from . import distributed
+    act = activation_code(activation)
+    key = (model, par, act)
+    layer = _RANK_LAYERS.get(key)
+    if layer is None or layer.m_cap < M:
+        if layer is not None:
+            _RANK_LAYERS.pop(key).close()
+        while len(_RANK_LAYERS) >= 2:
+            _RANK_LAYERS.pop(next(iter(_RANK_LAYERS))).close()
+        cap = 1 << max(0, int(max(M, 1) - 1).bit_length())
+        layer = distributed.init_layer(model, par, cap, w_local, activation=activation, knobs=knobs)
+        _RANK_LAYERS[key] = layer
+    layer.weights = w_local
+    if knobs is not None:
+        layer.knobs = knobs
+    return layer
+
+
 def execute_scheduled_rank(x_local, w_local: RankWeights, routing: RoutingTable, sched0: Optional[TileSchedule] = None,
                            sched1: Optional[TileSchedule] = None, activation: Activation = None,
                            combine_weights=None, layer: Optional["MoELayer"] = None, knobs: Optional[LayerKnobs] = None):
@@ -593,11 +721,7 @@ def execute_scheduled_rank(x_local, w_local: RankWeights, routing: RoutingTable,
     if layer is not None and layer.act != activation_code(activation):
         raise ConfigurationError("activation differs from the one the given layer was built with")
     if layer is None:
-        key = (routing.model, par, M, id(w_local), activation_code(activation))
-        layer = _RANK_LAYERS.get(key)
-        if layer is None:
-            layer = distributed.init_layer(routing.model, par, M, w_local, activation=activation, knobs=knobs)
-            _RANK_LAYERS[key] = layer
+        layer = _rank_layer(routing.model, par, M, w_local, activation, knobs)
     torch = layer.torch
     ex = torch.from_numpy(routing.as_array().copy())
     cw = None if combine_weights is None else torch.as_tensor(np.asarray(combine_weights, np.float32))

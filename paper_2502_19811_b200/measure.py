@@ -139,11 +139,11 @@ class EmulatedGroup:
     def _forward_timed(self, record: bool):
         """One forward, phase-ordered over the emulated ranks (ranks share a
         device, so each in-kernel wait is on work enqueued before it)."""
-        from .executor import fused_launch, index_flags
+        from .executor import index_flags
         torch = self.torch
         W = self.parallel.world_size
         ev = (lambda: torch.cuda.Event(enable_timing=True)) if record else (lambda: None)
-        fused = fused_launch(W, self.layers[0].n_comm1())
+        fused = self.layers[0].knobs.is_fused(W)
         rec = {k: [] for k in (("index", "layers", "finish") if fused else ("index", "layer0", "layer1", "finish"))}
 
         def timed(key, fn):

@@ -4,7 +4,7 @@ Every rank runs its own MoELayer (own CUDA context, own symmetric heap), the
 IPC handles are exchanged over gloo, and three consecutive forwards run
 concurrently across the processes -- the real multi-rank protocol (IPC-mapped
 peer heaps, system-scope epoch flags, dispatch pulls / combine pushes).  With
-COMET_SAME_DEVICE=1 all ranks share GPU 0 (COMET_GRID splits the SMs so the
+COMET_SAME_DEVICE=1 all ranks share GPU 0 (LayerKnobs.grid splits the SMs so the
 persistent kernels are co-resident).  Rank 0 checks the gathered output
 against the oracle (test infrastructure only)."""
 import os
@@ -34,9 +34,10 @@ def main():
     cw = np.random.default_rng(74).random((M, topk)).astype(np.float32)
     dev = distributed.local_device()
     rw = RankWeights.from_full(w.w0, w.w1, model, par, rank, device=dev)
-    grid = int(os.environ.get("COMET_GRID", 148))
+    grid = int(os.environ.get("COMET_TEST_GRID", 148))  # SMs per rank when ranks share one GPU
     layer = distributed.init_layer(model, par, M, rw, activation="tanh",
-                                   knobs=LayerKnobs(n_comm0=min(8, max(2, grid // 2 // 2 * 2))))
+                                   knobs=LayerKnobs(n_comm0=min(8, max(2, grid // 2 // 2 * 2)),
+                                                    grid=grid if grid < 148 else None))
     lo, hi = layer.token_range(M)
     ex = torch.from_numpy(routing.as_array().copy()).cuda(dev)
     outs = []

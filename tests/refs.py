@@ -18,22 +18,31 @@ def oracle_bf16_inputs(x, w0, w1, experts, activation=None, combine_weights=None
     return O.layer_forward_tp(*args, tp, activation=activation, combine_weights=combine_weights)
 
 
-def torch_reference(x, w0, w1, experts, activation=None, combine_w=None):
+def torch_reference(x, w0, w1, experts, activation=None, combine_w=None, tp=1):
     """Plain PyTorch fp32 reference of the same op (bf16 inputs, bf16 h and
-    expert rows -- the storage points of the fused kernels)."""
+    expert rows -- the storage points of the fused kernels).  ``tp`` > 1
+    follows execute_tp_sharded (ref executor.py:221-246): K is cut into tp
+    contiguous shards, each shard's expert row is its own bf16 partial, and
+    the partials are summed in shard order before the combine."""
     import torch
     M, N = x.shape
+    K = w0.shape[2]
+    ks = K // tp
     xf = x.to(torch.bfloat16).float()
     y = torch.zeros(M, N, dtype=torch.float32, device=x.device)
     for e in range(w0.shape[0]):
         tok, slot = (experts == e).nonzero(as_tuple=True)
         if tok.numel() == 0:
             continue
-        h = xf[tok] @ w0[e].to(torch.bfloat16).float()
-        if activation == "tanh":
-            h = torch.tanh(h)
-        h = h.to(torch.bfloat16).float()
-        ye = (h @ w1[e].to(torch.bfloat16).float()).to(torch.bfloat16).float()
+        ye = torch.zeros(tok.numel(), N, dtype=torch.float32, device=x.device)
+        for s in range(tp):
+            h = xf[tok] @ w0[e, :, s * ks:(s + 1) * ks].to(torch.bfloat16).float()
+            if activation == "tanh":
+                h = torch.tanh(h)
+            elif activation == "silu":
+                h = h * torch.sigmoid(h)
+            h = h.to(torch.bfloat16).float()
+            ye += (h @ w1[e, s * ks:(s + 1) * ks].to(torch.bfloat16).float()).to(torch.bfloat16).float()
         if combine_w is not None:
             ye = ye * combine_w[tok, slot][:, None]
         y.index_add_(0, tok, ye)

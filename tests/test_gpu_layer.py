@@ -85,18 +85,18 @@ def test_emulated_parallel_layouts_vs_oracle(tp, ep, std):
 
 
 @pytest.mark.parametrize("n_comm1", [0, 2, 6, "fused"])
-def test_combine_paths_agree(n_comm1, monkeypatch):
+def test_combine_paths_agree(n_comm1):
     """world 1: local combine kernel, combine CTAs, and the epilogue-fused
-    combine (COMET_FUSE1=1: last hosted row folds the earlier ones) agree."""
-    if n_comm1 == "fused":
-        monkeypatch.setenv("COMET_FUSE1", "1")
+    combine (LayerKnobs.fuse1: last hosted row folds the earlier ones) agree."""
+    fuse1 = n_comm1 == "fused"
+    if fuse1:
         n_comm1 = 0
     model = ModelConfig(L=1, E=8, topk=3, N=512, K=1024)
     routing = build_routing(model, ParallelSpec(), WorkloadSpec(M=777, seed=9, std=0.05))
     w = random_weights(model, seed=1)
     x = np.random.default_rng(2).standard_normal((777, 512))
     y = run_emulated(x, w, routing, ParallelSpec(), activation="tanh",
-                     knobs=LayerKnobs(n_comm1=n_comm1)).cpu().numpy()
+                     knobs=LayerKnobs(n_comm1=n_comm1, fuse1=fuse1)).cpu().numpy()
     ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), np.tanh)
     assert_close(y, ref, what=f"n_comm1={n_comm1}")
 
@@ -183,7 +183,7 @@ def test_mixtral_full_size_vs_torch_fp32_and_determinism():
 
 @pytest.mark.parametrize("tp,ep,topk,std", [(1, 1, 2, 0.032), (1, 4, 2, 0.05), (1, 8, 2, 0.0), (2, 2, 3, 0.032),
                                             (1, 2, 8, 0.0)])
-def test_launch_modes_bitwise_equal(tp, ep, topk, std, monkeypatch):
+def test_launch_modes_bitwise_equal(tp, ep, topk, std):
     """One fused launch for both layers (dynamic unit claims, layer1 tiles
     gated on per-tile H counters, dispatch CTAs joining the GEMMs) vs
     separate layer0 / layer1 launches, and every layer1 tail split: each
@@ -197,11 +197,9 @@ def test_launch_modes_bitwise_equal(tp, ep, topk, std, monkeypatch):
     x = np.random.default_rng(23).standard_normal((1500, 512))
     cw = np.random.default_rng(24).random((1500, topk))
     outs = []
-    for fused, split1 in (("0", "0"), ("1", "0"), ("1", "74"), ("1", "100000")):
-        monkeypatch.setenv("COMET_FUSED", fused)
-        monkeypatch.setenv("COMET_SPLIT1", split1)
+    for fused, split1 in ((False, 0), (True, 0), (True, 74), (True, 100000)):
         outs.append(run_emulated(x, w, routing, par, activation="silu", combine_weights=cw,
-                                 knobs=LayerKnobs(n_comm0=4, n_comm1=0)).cpu().numpy())
+                                 knobs=LayerKnobs(n_comm0=4, n_comm1=0, fused=fused, split1=split1)).cpu().numpy())
     for o in outs[1:]:
         np.testing.assert_array_equal(o, outs[0])
     silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
@@ -250,7 +248,7 @@ def test_narrow_last_blocks(tp, ep, n_comm1):
 
 
 @pytest.mark.parametrize("tp,ep,M", [(1, 8, 300), (1, 1, 200), (2, 4, 500), (1, 4, 64)])
-def test_split_k_small_m(tp, ep, M, monkeypatch):
+def test_split_k_small_m(tp, ep, M):
     """Few output tiles per rank -> split-K (fp32 partials, the last slice
     reduces in slice order): within tolerance of the oracle, run-to-run
     bitwise deterministic, and close to the unsplit path."""
@@ -261,10 +259,9 @@ def test_split_k_small_m(tp, ep, M, monkeypatch):
     x = np.random.default_rng(53).standard_normal((M, 512))
     cw = np.random.default_rng(54).random((M, 2))
     ys = []
-    for ks in ("8", "8", "0"):
-        monkeypatch.setenv("COMET_KSPLIT", ks)
+    for ks in (8, 8, 0):
         ys.append(run_emulated(x, w, routing, par, activation="gelu_tanh", combine_weights=cw,
-                               knobs=LayerKnobs(n_comm0=8, n_comm1=0)).cpu().numpy())
+                               knobs=LayerKnobs(n_comm0=8, n_comm1=0, ksplit_max=ks)).cpu().numpy())
     np.testing.assert_array_equal(ys[0], ys[1])
     gelu = lambda a: 0.5 * a * (1 + np.tanh(0.7978845608028654 * (a + 0.044715 * a ** 3)))  # noqa: E731
     ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), gelu, cw, tp=tp)
@@ -274,7 +271,7 @@ def test_split_k_small_m(tp, ep, M, monkeypatch):
 
 @pytest.mark.parametrize("E,topk,M,N,K", [(8, 2, 5000, 512, 1024), (8, 3, 3000, 512, 2048), (16, 4, 700, 256, 512),
                                           (8, 2, 100, 512, 2048)])
-def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
+def test_streamed_host_forward(E, topk, M, N, K):
     """comet_forward_host: upload chunks gate the dispatch, the fused combine
     (folder = each token's last-claimed row, all other rows folded) counts
     finished rows per chunk, downloads wait on the counts -- one launch.
@@ -284,7 +281,6 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     par = ParallelSpec()
     routing = build_routing(model, par, WorkloadSpec(M=M, seed=61, std=0.032))
     w = random_weights(model, seed=62)
-    monkeypatch.setenv("COMET_E2E", "stream")
     layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0),
                      activation="silu", knobs=LayerKnobs(n_comm0=16))
     x = torch.from_numpy(np.random.default_rng(63).standard_normal((M, N)).astype(np.float32)).to(torch.bfloat16)
@@ -293,7 +289,7 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     outs = []
     for _ in range(2):
         out = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
-        layer.forward_host(x.pin_memory(), ex.pin_memory(), cw.pin_memory(), out=out)
+        layer.forward_host(x.pin_memory(), ex.pin_memory(), cw.pin_memory(), out=out, mode="stream")
         torch.cuda.synchronize()
         outs.append(out)
     assert torch.equal(outs[0], outs[1])
@@ -310,7 +306,7 @@ def test_streamed_host_forward(E, topk, M, N, K, monkeypatch):
     (16, 4, 700, 512, 512, "1", "0", "8"), (8, 2, 100, 512, 2048, "1", "2", "8"),
     (8, 1, 1000, 512, 1024, "1", "2", "0"), (8, 2, 6000, 1024, 3200, "1", "3", "8"),
     (8, 2, 300, 512, 2048, "1", "0", "8"), (8, 2, 1, 512, 1024, "1", "3", "8"), (8, 4, 129, 512, 512, "1", "1", "4")])
-def test_zerocopy_host_forward(E, topk, M, N, K, dedup, ilv, dl, monkeypatch):
+def test_zerocopy_host_forward(E, topk, M, N, K, dedup, ilv, dl):
     """comet_forward_zerocopy: dispatch CTAs read token rows from pinned host
     memory (once per token with dedup, fanned out to every hosted row), the
     fused combine writes output rows straight to pinned host memory; layer1
@@ -324,11 +320,8 @@ def test_zerocopy_host_forward(E, topk, M, N, K, dedup, ilv, dl, monkeypatch):
     par = ParallelSpec()
     routing = build_routing(model, par, WorkloadSpec(M=M, seed=71, std=0.032))
     w = random_weights(model, seed=72)
-    monkeypatch.setenv("COMET_ZC_DEDUP", dedup)
-    monkeypatch.setenv("COMET_ZC_ILV", ilv)
-    monkeypatch.setenv("COMET_ZC_DL", dl)
-    layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0),
-                     activation="silu", knobs=LayerKnobs(n_comm0=16))
+    layer = MoELayer(model, par, 0, M, RankWeights.from_full(w.w0, w.w1, model, par, 0), activation="silu",
+                     knobs=LayerKnobs(n_comm0=16, zc_dedup=dedup == "1", zc_interleave=int(ilv), zc_download=int(dl)))
     x = torch.from_numpy(np.random.default_rng(73).standard_normal((M, N)).astype(np.float32)).to(torch.bfloat16)
     ex = torch.from_numpy(routing.as_array().copy())
     cw = torch.from_numpy(np.random.default_rng(74).random((M, topk)).astype(np.float32))
@@ -346,8 +339,8 @@ def test_zerocopy_host_forward(E, topk, M, N, K, dedup, ilv, dl, monkeypatch):
 
 
 @pytest.mark.parametrize("E,topk,tp,ep,M", [(16, 4, 1, 4, 3000), (64, 8, 1, 8, 2000), (8, 2, 2, 4, 4000)])
-def test_dispatch_dedup_bitwise(E, topk, tp, ep, M, monkeypatch):
-    """Per-token dedup of the NVLink pulls (COMET_DEDUP=1, dispatch_rows_dedup:
+def test_dispatch_dedup_bitwise(E, topk, tp, ep, M):
+    """Per-token dedup of the NVLink pulls (LayerKnobs.dedup=1, dispatch_rows_dedup:
     one read per (token, rank), fanned out to its hosted rows) moves the same
     bytes into the same rows: bitwise equal to the per-row dispatch, and
     within tolerance of the oracle."""
@@ -358,10 +351,9 @@ def test_dispatch_dedup_bitwise(E, topk, tp, ep, M, monkeypatch):
     x = np.random.default_rng(83).standard_normal((M, 512))
     cw = np.random.default_rng(84).random((M, topk))
     outs = []
-    for dd in ("0", "1", "1"):
-        monkeypatch.setenv("COMET_DEDUP", dd)
+    for dd in (0, 1, 1):
         outs.append(run_emulated(x, w, routing, par, activation="silu", combine_weights=cw,
-                                 knobs=LayerKnobs(n_comm0=8, n_comm1=0)).cpu().numpy())
+                                 knobs=LayerKnobs(n_comm0=8, n_comm1=0, dedup=dd)).cpu().numpy())
     np.testing.assert_array_equal(outs[1], outs[0])
     np.testing.assert_array_equal(outs[2], outs[0])
     silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731

@@ -1,7 +1,7 @@
 """The multi-rank protocol with real processes: one process (own CUDA
 context and symmetric heap) per rank, IPC-mapped peer heaps, forwards running
 concurrently -- on a single-GPU box every rank shares GPU 0 with the SMs split
-between the ranks' persistent kernels (COMET_GRID)."""
+between the ranks' persistent kernels (LayerKnobs.grid)."""
 
 import os
 import subprocess
@@ -18,7 +18,7 @@ def test_processes_share_the_protocol(tp, ep, topk):
     import torch
     world = tp * ep
     grid = torch.cuda.get_device_properties(0).multi_processor_count // world // 2 * 2
-    env = dict(os.environ, COMET_SAME_DEVICE="1", COMET_GRID=str(grid), MASTER_ADDR="127.0.0.1")
+    env = dict(os.environ, COMET_SAME_DEVICE="1", COMET_TEST_GRID=str(grid), MASTER_ADDR="127.0.0.1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + tp * 100 + ep * 10 + topk),
            os.path.join(ROOT, "tests", "mp_worker.py"), str(tp), str(ep), str(topk)]
