@@ -24,7 +24,9 @@ line range it follows under ``/root/reference/pkg/src/moepipe/``:
 * float path: ``layer_forward`` = ``execute_naive`` (executor.py:132-148) with
   ``_hidden_row`` (86-90), ``_output_columns`` (93-99) and ``_combine``
   (102-120) folded into one GEMM pair per expert; ``layer_forward_tp`` =
-  ``execute_tp_sharded`` (executor.py:221-246).
+  ``execute_tp_sharded`` (executor.py:221-246); ``execute_naive_literal`` =
+  the reference's loop nest itself (one dot per (token, expert) hidden row
+  and per output column), the literal CPU arm at Config 1.
 
 Pinning: ``tests/test_oracle_golden.py`` checks every function here against
 ``tests/golden/*`` -- fixtures produced by running the reference package
@@ -218,6 +220,35 @@ def layer_forward(x: np.ndarray, w0: np.ndarray, w1: np.ndarray, experts: np.nda
     if experts.shape[0] == 0:
         return np.zeros((0, x.shape[1]), dtype=dtype)
     return _fold_combine(experts, rows, pos, combine_weights, dtype)
+
+
+def execute_naive_literal(x: np.ndarray, w0: np.ndarray, w1: np.ndarray, experts: np.ndarray,
+                          activation: Activation = None,
+                          combine_weights: Optional[np.ndarray] = None) -> np.ndarray:
+    """The reference's ``execute_naive`` loop nest restated literally
+    (executor.py:132-148): token-major, per (token, expert) ``_hidden_row``
+    = one ``np.dot`` of the token row with w0[e] (86-90), ``_output_columns``
+    = one ``np.dot`` per output column (93-99), and ``_combine``'s
+    ascending-slot fold (102-120).  Same float64 operations in the same
+    order, so it reproduces the reference output bitwise; it is the CPU
+    timing arm at Config 1 (524K dot calls, seconds)."""
+    x = np.asarray(x, dtype=np.float64)
+    m, n = x.shape
+    out = np.zeros((m, n), dtype=np.float64)
+    for t in range(m):
+        acc = None
+        for slot, e in enumerate(experts[t]):
+            h = np.dot(x[t], w0[e])
+            if activation is not None:
+                h = activation(h)
+            w1_e = w1[e]
+            row = np.array([np.dot(h, w1_e[:, j]) for j in range(n)], dtype=np.float64)
+            if combine_weights is not None:
+                row = row * combine_weights[t, slot]
+            acc = row.copy() if acc is None else acc + row
+        if acc is not None:
+            out[t] = acc
+    return out
 
 
 def layer_forward_tp(x, w0, w1, experts, tp: int, activation: Activation = None,

@@ -130,9 +130,10 @@ class RankWeights:
         s = parallel.tp_index_of_rank(rank)
         n_pad, k_pad = _ceil(model.N, 64), _ceil(kl, 64)
         dev = torch.device("cuda", device)
-        w0s = torch.as_tensor(np.asarray(w0[e_lo:e_lo + e_per, :, s * kl:(s + 1) * kl])) \
+        # (numpy: a private copy of this rank's slice -- cached weights are read-only)
+        w0s = torch.from_numpy(np.array(w0[e_lo:e_lo + e_per, :, s * kl:(s + 1) * kl])) \
             if not isinstance(w0, torch.Tensor) else w0[e_lo:e_lo + e_per, :, s * kl:(s + 1) * kl]
-        w1s = torch.as_tensor(np.asarray(w1[e_lo:e_lo + e_per, s * kl:(s + 1) * kl, :])) \
+        w1s = torch.from_numpy(np.array(w1[e_lo:e_lo + e_per, s * kl:(s + 1) * kl, :])) \
             if not isinstance(w1, torch.Tensor) else w1[e_lo:e_lo + e_per, s * kl:(s + 1) * kl, :]
         w0t = torch.zeros(e_per, k_pad, n_pad, dtype=torch.bfloat16, device=dev)
         w1t = torch.zeros(e_per, n_pad, k_pad, dtype=torch.bfloat16, device=dev)

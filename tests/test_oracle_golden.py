@@ -143,3 +143,26 @@ def test_round_bf16_matches_torch():
     ours = O.round_bf16(a)
     theirs = torch.from_numpy(a).to(torch.bfloat16).float().numpy()
     np.testing.assert_array_equal(ours, theirs)
+
+
+def test_literal_execute_naive_reproduces_reference_bitwise():
+    """The literal loop-nest restatement (the Config-1 CPU timing arm) gives
+    the reference's own execute_naive output bitwise (at the fixture's
+    float32 storage precision) on a slice of Config 1
+    (same float64 operations in the same order), and a weighted / tanh small
+    case equal to the vectorised oracle within fp64 rounding."""
+    z = np.load(os.path.join(GOLD, "layer_c1.npz"))
+    model = C.ModelConfig(L=1, E=8, topk=2, N=512, K=1024)
+    r = Rt.build_routing(model, C.ParallelSpec(1, 8), C.WorkloadSpec(M=512, seed=0))
+    x = np.random.default_rng(1).standard_normal((512, 512))
+    rng = np.random.default_rng(2)
+    scale = 1.0 / np.sqrt(512)
+    w0 = rng.standard_normal((8, 512, 1024)) * scale
+    w1 = rng.standard_normal((8, 1024, 512)) * scale
+    ex = r.as_array()
+    y = O.execute_naive_literal(x[:24], w0, w1, ex[:24])
+    np.testing.assert_array_equal(y.astype(np.float32), z["y"][:24])  # fixture stored as float32
+    cw = np.random.default_rng(3).random((24, 2))
+    y2 = O.execute_naive_literal(x[:24], w0, w1, ex[:24], activation=np.tanh, combine_weights=cw)
+    ref = O.layer_forward(x[:24], w0, w1, ex[:24], activation=np.tanh, combine_weights=cw)
+    np.testing.assert_allclose(y2, ref, rtol=1e-12, atol=1e-12)
