@@ -20,9 +20,12 @@ region (one GPU: the zero-copy forward, dispatch CTAs read the tokens from
 pinned host memory and the fused combine writes the output there; multi-GPU:
 copy, forward, copy).
 ``--impl reference`` times the reference algorithm on the host cores (the
-numpy oracle port; the reference package itself is pure Python and cannot
-run a Mixtral layer in bounded time) on a bounded token sample per step,
-extrapolated to the full workload.
+numpy oracle port, fp32, every host core; the reference package itself is
+pure Python and its literal loop nest would take ~6 h per Mixtral layer) on
+the FULL workload every step (no sampling, no extrapolation), plus the
+literal execute_naive loop nest once at Config 1.  ``roofline`` times the
+layer kernel alone with CUDA events inside the same timed steps as
+``value``.
 """
 
 from __future__ import annotations
@@ -160,19 +163,9 @@ def barrier(world: int):
     torch.cuda.synchronize()
 
 
-def cpu_reference_sample(model, routing, sample_tokens: int, steps: int, warmup: int):
-    """Reference algorithm (oracle.moe_oracle.layer_forward: execute_naive
-    restated with one GEMM pair per expert) on the host cores, fp32, over the
-    first ``sample_tokens`` tokens; returns (ms per full-workload step, info)."""
-    import numpy as np
-    from oracle import moe_oracle as O
-    rng = np.random.default_rng(11)
-    w0 = rng.standard_normal((model.E, model.N, model.K), dtype=np.float32) / np.float32(math.sqrt(model.N))
-    w1 = rng.standard_normal((model.E, model.K, model.N), dtype=np.float32) / np.float32(math.sqrt(model.N))
-    x = rng.standard_normal((sample_tokens, model.N), dtype=np.float32)
-    ex = routing.as_array()[:sample_tokens]
-    # every host core for the BLAS pool (torchrun exports OMP_NUM_THREADS=1 to
-    # multi-rank jobs, which OpenBLAS would otherwise honour)
+def _blas_threads():
+    """Every host core for the BLAS pool (torchrun exports OMP_NUM_THREADS=1
+    to multi-rank jobs, which OpenBLAS would otherwise honour)."""
     import contextlib
     limits, threads = contextlib.nullcontext(), os.cpu_count()
     try:
@@ -182,6 +175,40 @@ def cpu_reference_sample(model, routing, sample_tokens: int, steps: int, warmup:
         threads = max([i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"] or [n_host])
     except Exception:
         pass
+    return limits, threads
+
+
+def _cpu_weights(model, dtype):
+    """Random N(0,1)/sqrt(N) expert weights [E,N,K] / [E,K,N] for the CPU arm,
+    tiled from one 16 Mi-value random block (values do not change the
+    timing; generating 2 x 940 M normals would take longer than the run)."""
+    import numpy as np
+    rng = np.random.default_rng(11)
+    block = (rng.standard_normal(1 << 24, dtype=np.float32) / np.float32(math.sqrt(model.N))).astype(dtype)
+    n = model.E * model.N * model.K
+    reps = -(-n // block.size)
+    w0 = np.tile(block, reps)[:n].reshape(model.E, model.N, model.K)
+    w1 = np.tile(block[::-1], reps)[:n].reshape(model.E, model.K, model.N)
+    return w0, w1
+
+
+def cpu_reference(model, routing, steps: int, warmup: int, c1_literal: bool = True):
+    """The reference algorithm on the host cores over the FULL workload (all
+    M tokens, every expert, full N and K; fp32 numpy/OpenBLAS):
+    oracle.moe_oracle.layer_forward = execute_naive (executor.py:132-148)
+    restated with one GEMM pair per expert.  No extrapolation: each step is
+    one whole layer forward.  With ``c1_literal`` also times the literal
+    execute_naive loop nest (oracle.execute_naive_literal, bitwise equal to
+    the reference) once at BASELINE Config 1 (E=8 top-2, M=512, N=512,
+    K=1024).  Returns (median ms per step, info)."""
+    import numpy as np
+    from oracle import moe_oracle as O
+    w0, w1 = _cpu_weights(model, np.float32)
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((routing.workload.M, model.N), dtype=np.float32)
+    ex = routing.as_array()
+    limits, threads = _blas_threads()
+    c1_ms = None
     with limits:
         for _ in range(max(0, warmup)):
             O.layer_forward(x, w0, w1, ex, dtype=np.float32)
@@ -190,16 +217,29 @@ def cpu_reference_sample(model, routing, sample_tokens: int, steps: int, warmup:
             t0 = time.perf_counter()
             O.layer_forward(x, w0, w1, ex, dtype=np.float32)
             times.append(time.perf_counter() - t0)
-    scale = routing.workload.M / sample_tokens
-    ms = statistics.median(times) * 1e3 * scale
+        if c1_literal:
+            from paper_2502_19811_b200 import ModelConfig, ParallelSpec, WorkloadSpec, build_routing
+            c1 = ModelConfig(L=1, E=8, topk=2, N=512, K=1024)
+            r1 = build_routing(c1, ParallelSpec(tp=1, ep=8), WorkloadSpec(M=512, seed=0, std=0.0))
+            g = np.random.default_rng(1)
+            x1 = g.standard_normal((512, 512))
+            w01 = g.standard_normal((8, 512, 1024)) / math.sqrt(512)
+            w11 = g.standard_normal((8, 1024, 512)) / math.sqrt(512)
+            t0 = time.perf_counter()
+            O.execute_naive_literal(x1, w01, w11, r1.as_array())
+            c1_ms = (time.perf_counter() - t0) * 1e3
+    del w0, w1
     try:
         import torch
         torch_threads = torch.get_num_threads()
     except Exception:
         torch_threads = None
-    return ms, {"cores": os.cpu_count(), "threads": threads, "torch_threads": torch_threads,
-                "sample": f"{sample_tokens} of {routing.workload.M} tokens (all experts, full N/K), fp32 numpy "
-                          f"(OpenBLAS), median of {steps} steps, scaled x{scale:g} to the full workload"}
+    return statistics.median(times) * 1e3, {
+        "cores": os.cpu_count(), "threads": threads, "torch_threads": torch_threads, "times_ms": times,
+        "c1_literal_execute_naive_ms": None if c1_ms is None else round(c1_ms, 1),
+        "sample": f"the full workload every step ({routing.workload.M} tokens, all {model.E} experts, full N/K), "
+                  f"fp32 numpy (OpenBLAS, {threads} threads), median of {steps} steps after {warmup} warm-up; "
+                  f"no extrapolation"}
 
 
 def run_reference(args):
@@ -209,17 +249,23 @@ def run_reference(args):
     from paper_2502_19811_b200 import ModelConfig, ParallelSpec, WorkloadSpec, build_routing
     E, topk, N, K, tp = SHAPES[args.shape]
     model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
-    ep = max(1, args.gpus // tp) if args.gpus >= tp else 1
-    routing = build_routing(model, ParallelSpec(tp=1, ep=1), WorkloadSpec(M=args.M, seed=0, std=args.std))
-    ms, info = cpu_reference_sample(model, routing, args.cpu_sample, args.steps, args.warmup)
+    if args.gpus % tp:
+        tp = 1
+    ep = args.gpus // tp
+    routing = build_routing(model, ParallelSpec(tp=tp, ep=ep), WorkloadSpec(M=args.M, seed=0, std=args.std))
+    # one CPU warm-up step (first-touch of the weights); the GPU-style W
+    # warm-up would only repeat the same BLAS calls
+    warm = min(args.warmup, 1)
+    ms, info = cpu_reference(model, routing, args.steps, warm)
     out = {
         "impl": "reference", "metric": "moe_layer_fwd_latency", "value": round(ms, 3), "unit": "ms",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": warm, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args, model, ep, tp),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": info["threads"], "kind": "port",
                          "sample": info["sample"], "host_cpu_count": info["cores"], "blas_threads": info["threads"],
-                         "torch_threads": info["torch_threads"]},
+                         "torch_threads": info["torch_threads"],
+                         "c1_literal_execute_naive_ms": info["c1_literal_execute_naive_ms"]},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
@@ -291,6 +337,12 @@ def run_ours(args):
         step()
     barrier(world)
     # ---- timed region (device events, max over ranks) ----
+    # The library brackets every layer-kernel launch (moe_layer_kernel) of the
+    # timed steps with a CUDA event pair on the launch stream
+    # (comet_kernel_timing_*), so the roofline's kernel time comes from the
+    # same window as ``value``.
+    ctx = layer.ctx
+    ctx.kernel_timing_enable(2 * args.steps)
     with ClockSampler(local) as clk:
         clk.wait_started()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -300,35 +352,22 @@ def run_ours(args):
             step()
         e.record(stream)
         barrier(world)
-        ms_local = s.elapsed_time(e) / args.steps
-        # per-kernel durations (same stream), for the roofline of the dominant kernel
-        from paper_2502_19811_b200.executor import fused_launch
-        ctx = layer.ctx
-        fused = fused_launch(world, layer.n_comm1())
-        n_prof = max(3, min(args.steps, 10))
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_prof)]
-        for i in range(n_prof):
-            ctx.index_build(ex, M, flags=index_flags(world, layer.n_comm1()))
-            ev[i][0].record(stream)
-            if fused:
-                ctx.layers(layer.weights.w0t, layer.weights.w1t, None, y, layer.act,
-                           knobs.n_comm0 if world > 1 else 0, knobs.group0, knobs.wave1)
-                ev[i][1].record(stream)
-            else:
-                ctx.layer0(layer.weights.w0t, layer.act, knobs.n_comm0 if world > 1 else 0, knobs.group0)
-                ev[i][1].record(stream)
-                ctx.layer1(layer.weights.w1t, None, y, layer.n_comm1(), knobs.wave1)
-            ev[i][2].record(stream)
-            ctx.combine_finish(y)
-            ev[i][3].record(stream)
-        barrier(world)
+    ms_local = s.elapsed_time(e) / args.steps
+    k_times = ctx.kernel_timing_read()
+    ctx.kernel_timing_enable(0)
+    fused = layer.knobs.is_fused(world)
     ms = max_over_ranks(ms_local, world)
-    t_l0 = statistics.median(ev[i][0].elapsed_time(ev[i][1]) for i in range(n_prof))
-    t_l1 = statistics.median(ev[i][1].elapsed_time(ev[i][2]) for i in range(n_prof))
+    if len(k_times) != args.steps * (1 if fused else 2):
+        raise SystemExit(f"kernel timing recorded {len(k_times)} launches for {args.steps} steps")
+    # per step: one launch (fused) or layer0 + layer1 launches
+    per_step = [sum(k_times[i:i + (1 if fused else 2)]) for i in range(0, len(k_times), 1 if fused else 2)]
+    t_kernel_local = statistics.mean(per_step)
+    t_kernel = max_over_ranks(t_kernel_local, world)
+    if t_kernel_local > ms_local * 1.0005:
+        raise SystemExit(f"layer kernel {t_kernel_local:.4f} ms > step {ms_local:.4f} ms: timing is inconsistent")
     meta = ctx.index_meta()
     rows = int(meta[0])
     kl = K // tp
-    flops_layer = 2.0 * rows * N * kl  # one GEMM of the pair (algorithmic, unpadded rows)
 
     # ---- e2e: public per-rank API with host (pinned) buffers ----
     x_host = x_local.cpu().pin_memory()
@@ -374,27 +413,30 @@ def run_ours(args):
     # ---- roofline ----
     peak_burst, peak_sust, hbm_gbs, peak_src = load_peaks()
     rows_max = max_over_ranks(float(rows), world)
-    t_flops_ms = 2 * (2.0 * rows_max * N * kl) / (peak_burst * 1e12) * 1e3
-    t_flops_sust_ms = 2 * (2.0 * rows_max * N * kl) / (peak_sust * 1e12) * 1e3
-    # the per-kernel timing runs right after the long timed loop: sustained peak
-    peak_tf = peak_sust
-    if fused:  # one launch runs both GEMMs (layer0 + layer1)
-        dominant, t_dom, flops_dom = "layers", t_l0, 2 * flops_layer
-    else:
-        dominant = "layer1" if t_l1 >= t_l0 else "layer0"
-        t_dom, flops_dom = max(t_l0, t_l1), flops_layer
-    achieved_tf = flops_dom / (t_dom * 1e-3) / 1e12
-    traffic = load_traffic(dominant)
+    flops_step = 2 * (2.0 * rows_max * N * kl)  # two GEMMs, 2 flop / MAC, hottest rank
+    window_s = ms * args.steps * 1e-3
+    # MEASURED_PEAKS: the burst figure for a kernel timed in a short window,
+    # the sustained one (4 s back to back) for a long one
+    peak_tf, peak_kind = (peak_burst, "burst") if window_s < 1.0 else (peak_sust, "sustained")
+    t_flops_ms = flops_step / (peak_tf * 1e12) * 1e3
+    t_flops_burst_ms = flops_step / (peak_burst * 1e12) * 1e3
+    t_flops_sust_ms = flops_step / (peak_sust * 1e12) * 1e3
+    flops_launch = 2 * (2.0 * rows * N * kl)  # this rank's launch(es) of one step
+    achieved_tf = flops_launch / (t_kernel_local * 1e-3) / 1e12
+    traffic = load_traffic("layers" if fused else "layer1")
+    bytes_step = comm_bytes(routing, par, rank, N)
     launches_per_step = (4 if fused else 5) - (0 if (world == 1 and knobs.n_comm1 == 0) else 1) + \
         (1 if world > 1 else 0)
     clocks = clk.summary()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cms, info = cpu_reference_sample(model, routing, args.cpu_sample, 3, 1)
+        # bounded: 3 full-workload steps (~15 s on 16 cores) + the C1 literal loop
+        cms, info = cpu_reference(model, routing, 3, 1)
         cpu = {"value": round(cms, 3), "unit": "ms", "cores": info["threads"], "kind": "port",
                "sample": info["sample"], "host_cpu_count": info["cores"], "blas_threads": info["threads"],
-               "torch_threads": info["torch_threads"]}
+               "torch_threads": info["torch_threads"],
+               "c1_literal_execute_naive_ms": info["c1_literal_execute_naive_ms"]}
 
     if rank == 0:
         out = {
@@ -404,17 +446,24 @@ def run_ours(args):
             "data": "synthetic tokens, random-init weights", "config": workload_config(args, model, ep, tp),
             "pct_of_roofline": round(100.0 * t_flops_ms / ms, 2),
             "roofline_ms": round(t_flops_ms, 4),
+            "pct_of_roofline_burst": round(100.0 * t_flops_burst_ms / ms, 2),
             "pct_of_roofline_sustained": round(100.0 * t_flops_sust_ms / ms, 2),
-            "pct_of_roofline_spec_2250tf": round(100.0 * t_flops_ms * peak_burst / 2250.0 / ms, 2),
-            "roofline_note": "roofline_ms = 2 GEMMs x 2*rows*N*K/tp FLOP at the measured burst bf16 peak "
-                             "(BASELINE.md); pct_of_roofline_sustained uses the measured sustained peak",
+            "pct_of_roofline_spec_2250tf": round(100.0 * flops_step / 2250e12 * 1e3 / ms, 2),
+            "roofline_note": f"roofline_ms = 2 GEMMs x 2*rows*N*K/tp FLOP of the hottest rank at the measured "
+                             f"{peak_kind} bf16 peak (timed window {window_s:.3f} s; burst below 1 s); "
+                             f"NVLink term {bytes_step['t_nvlink_ms']} ms",
             "roofline": {"bound": "tensor",
-                         "kernel": "moe_layer_kernel (" + ("layer0 + layer1, one launch" if fused else dominant) + ")",
+                         "kernel": "moe_layer_kernel (" + ("layer0 + layer1, one launch" if fused
+                                                           else "layer0 + layer1 launches") + ")",
                          "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
-                         "peak_source": peak_src + ", sustained figure (kernel timed inside a long step)",
-                         "flops_per_launch": flops_dom, "ms_per_launch": round(t_dom, 4)},
-            "kernels_ms": ({"layers": round(t_l0, 4)} if fused else {"layer0": round(t_l0, 4), "layer1": round(t_l1, 4)}),
+                         "peak_source": f"{peak_src}, {peak_kind} figure",
+                         "flops_per_launch": flops_launch, "ms_per_launch": round(t_kernel_local, 4),
+                         "timing": f"CUDA events around each of the {len(k_times)} layer-kernel launches of the "
+                                   f"timed steps, on the launch stream (comet_kernel_timing_*); mean",
+                         "kernel_share_of_step": round(t_kernel_local / ms_local, 4)},
+            "kernels_ms": {"layers": round(t_kernel, 4), "step": round(ms, 4)},
+            "comm_bytes_per_step": bytes_step,
             "unfused_ms": None if unfused_ms is None else round(unfused_ms, 4),
             "speedup_vs_unfused": None if unfused_ms is None else round(unfused_ms / ms, 3),
             **({"unfused_error": unfused_error} if unfused_error else {}),
@@ -437,6 +486,31 @@ def run_ours(args):
     return 0
 
 
+def comm_bytes(routing, par, rank, N):
+    """Dispatch / combine bytes of one step on this rank:
+    distinct (token, remote rank) pairs x 2N bytes each way (the
+    deduplicated all-to-allv), and the rows the per-row dispatch actually
+    pulls.  Zero at world 1 (every row is HBM-local)."""
+    import numpy as np
+    from paper_2502_19811_b200.measure import NVLINK_GBS as nvl, distinct_remote_pairs
+    if par.world_size == 1:
+        return {"dispatch_in": 0, "combine_out": 0, "dispatch_pulled": 0, "t_nvlink_ms": 0.0}
+    d_out, d_in = distinct_remote_pairs(routing)
+    ex = routing.as_array()
+    M, W = ex.shape[0], par.world_size
+    e_per = routing.model.E // par.ep
+    base = M // W
+    src = np.minimum(np.arange(M) // base, W - 1) if base else np.full(M, W - 1)
+    g = rank // par.tp
+    hosted = (ex // e_per == g)
+    pulled = int((hosted & (src[:, None] != rank)).sum())
+    b = 2 * N
+    byts = 2.0 * N * (d_out + d_in)
+    return {"dispatch_in": int(d_in[rank]) * b, "combine_out": int(d_in[rank]) * b,
+            "dispatch_pulled": pulled * b,
+            "t_nvlink_ms": round(float(byts.max()) / (nvl * 1e9) * 1e3, 4)}
+
+
 def load_traffic(dominant):
     """dram read+write bytes per launch of the dominant kernel from the
     committed ncu --set full summary (profiles/), or None."""
@@ -452,8 +526,8 @@ def load_traffic(dominant):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--shape", choices=sorted(SHAPES), default="mixtral-8x7b")
     ap.add_argument("--M", type=int, default=8192)
@@ -464,7 +538,6 @@ def main():
     ap.add_argument("--group0", type=int, default=None,
                     help="layer0 pair-group raster (default: 8 at EP=1 and EP>=8, 4 at EP=2/4; measured)")
     ap.add_argument("--wave1", type=int, default=4)
-    ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
     args = ap.parse_args()

@@ -193,6 +193,16 @@ int32_t comet_hidden_rows_cap(comet_ctx* ctx);
 int comet_timeline_enable(comet_ctx* ctx, int cap);
 int comet_timeline_dump(comet_ctx* ctx, void* host_buf, size_t cap_bytes);
 
+/* Launch timing of the layer kernel (moe_layer_kernel) alone: with `slots`
+ * > 0, the next `slots` launches are bracketed by a cudaEvent pair recorded
+ * on their launch stream (so the duration excludes the index build, the
+ * local dispatch / combine kernels and host gaps).  read waits for the
+ * recorded launches, writes min(cap, recorded) durations in ms to ms_out,
+ * stores the count in *n_out and re-arms the ring.  0 slots disables.
+ * Measurement aid for bench.py's roofline (no reference counterpart). */
+int comet_kernel_timing_enable(comet_ctx* ctx, int slots);
+int comet_kernel_timing_read(comet_ctx* ctx, float* ms_out, int cap, int* n_out);
+
 /* GPU router front-end (no context).  Gate logits [M, E] (logits_dtype 0 =
  * fp32, 1 = bf16, row-major, device) -> d_experts [M, topk] int32, the top-k
  * expert ids stored ASCENDING per token: the reference router-output layout

@@ -33,7 +33,8 @@ EXPORTS = (
     "comet_signal_tokens_ready", "comet_layer0", "comet_layer1", "comet_layers", "comet_combine_finish", "comet_forward",
     "comet_hidden_buffer", "comet_yrows_buffer", "comet_hidden_rows_cap", "comet_device_info",
     "comet_timeline_enable", "comet_timeline_dump", "comet_router_topk", "comet_forward_host", "comet_forward_zerocopy",
-    "comet_set_option", "comet_get_option", "comet_abort_waits",
+    "comet_set_option", "comet_get_option", "comet_abort_waits", "comet_kernel_timing_enable",
+    "comet_kernel_timing_read",
 )
 
 # Per-context kernel options (include/comet_b200.h COMET_OPT_*).
@@ -107,6 +108,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "comet_forward": ([vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp], i32),
         "comet_device_info": ([i32, _P32], i32),
         "comet_timeline_enable": ([vp, i32], i32),
+        "comet_kernel_timing_enable": ([vp, i32], i32),
+        "comet_kernel_timing_read": ([vp, vp, i32, vp], i32),
         "comet_timeline_dump": ([vp, vp, c.c_size_t], i32),
         "comet_router_topk": ([vp, i32, i32, i32, i32, i32, vp, vp, vp], i32),
         "comet_forward_host": ([vp, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, i32, vp], i32),
@@ -336,6 +339,20 @@ class Context:
             self.handle, vp(x_host.data_ptr()), vp(experts_host.data_ptr()),
             vp(combine_w_host.data_ptr()) if combine_w_host is not None else None, vp(y_host.data_ptr()), M,
             vp(w0t.data_ptr()), vp(w1t.data_ptr()), activation, n_comm0, group0, wave1, vp(self._stream(stream))))
+
+    def kernel_timing_enable(self, slots: int) -> None:
+        """Bracket the next ``slots`` layer-kernel launches with CUDA events."""
+        self._kt_slots = slots
+        check(self.lib.comet_kernel_timing_enable(self.handle, slots))
+
+    def kernel_timing_read(self):
+        """Durations (ms) of the timed layer-kernel launches since enable/read."""
+        cap = max(1, getattr(self, "_kt_slots", 0))
+        buf = np.zeros(cap, dtype=np.float32)
+        n = ctypes.c_int(0)
+        check(self.lib.comet_kernel_timing_read(self.handle, buf.ctypes.data_as(ctypes.c_void_p), cap,
+                                                ctypes.byref(n)))
+        return buf[:n.value].tolist()
 
     def timeline_enable(self, cap: int) -> None:
         self._tl_cap = cap

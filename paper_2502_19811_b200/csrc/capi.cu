@@ -190,6 +190,10 @@ struct comet_ctx {
   float* part = nullptr;       // split-K partials: 2 layers x (pairs x 2 CTA tiles) x 128 x 512 fp32
   uint32_t* split_cnt = nullptr;  // 2 layers x 512 slice counters (reset by each tile's finisher)
   int n_h = 0;
+  // layer-kernel launch timing (comet_kernel_timing_*): an event pair around
+  // each moe_layer_kernel launch, on the launch stream, in a ring of slots
+  std::vector<cudaEvent_t> kt_ev;
+  int kt_slots = 0, kt_next = 0;
 };
 
 cudaError_t set_abort_flag_index(const volatile uint32_t* p);
@@ -457,6 +461,7 @@ int comet_ctx_destroy(comet_ctx* x) {
   if (x->ev_start) cudaEventDestroy(x->ev_start);
   if (x->ev_index) cudaEventDestroy(x->ev_index);
   if (x->ev_down) cudaEventDestroy(x->ev_down);
+  for (cudaEvent_t e : x->kt_ev) cudaEventDestroy(e);
   cudaFree(x->part);
   cudaFree(x->split_cnt);
   cudaFree(x->timeline);
@@ -778,7 +783,10 @@ static int launch_kernel(comet_ctx* x, KernelArgs& f, const CUtensorMap& a0, con
   at[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = (x->opt[COMET_OPT_PDL] & 2) ? 2 : 1;
+  const bool timed = x->kt_slots > 0 && x->kt_next < x->kt_slots;
+  if (timed) CK(cudaEventRecord(x->kt_ev[2 * x->kt_next], st));
   CK(cudaLaunchKernelEx(&lc, moe_layer_kernel, a0, b0, a1, b1, x->tm_Hs, x->tm_ys, f));
+  if (timed) CK(cudaEventRecord(x->kt_ev[2 * x->kt_next++ + 1], st));
   return COMET_OK;
 }
 
@@ -941,6 +949,29 @@ int comet_layers(comet_ctx* x, const void* w0t, const void* w1t, const float* co
   if (int rc = local_combine(x, f.l[1], combine_w, y_local, st)) return rc;
   x->last_y = y_local;
   x->last_combine_w = combine_w;
+  return COMET_OK;
+}
+
+int comet_kernel_timing_enable(comet_ctx* x, int slots) {
+  if (slots < 0) return fail(COMET_EINVAL, "slots=%d must be >= 0", slots);
+  CK(cudaSetDevice(x->cfg.device));
+  for (cudaEvent_t e : x->kt_ev) cudaEventDestroy(e);
+  x->kt_ev.assign(2 * (size_t)slots, nullptr);
+  for (auto& e : x->kt_ev) CK(cudaEventCreate(&e));
+  x->kt_slots = slots;
+  x->kt_next = 0;
+  return COMET_OK;
+}
+
+int comet_kernel_timing_read(comet_ctx* x, float* ms_out, int cap, int* n_out) {
+  CK(cudaSetDevice(x->cfg.device));
+  const int n = std::min(cap, x->kt_next);
+  for (int i = 0; i < n; ++i) {
+    CK(cudaEventSynchronize(x->kt_ev[2 * i + 1]));
+    CK(cudaEventElapsedTime(&ms_out[i], x->kt_ev[2 * i], x->kt_ev[2 * i + 1]));
+  }
+  if (n_out) *n_out = n;
+  x->kt_next = 0;  // re-arm
   return COMET_OK;
 }
 

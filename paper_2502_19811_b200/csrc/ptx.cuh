@@ -399,7 +399,10 @@ struct Spin {
     } else if (t - t0 > g_spin_timeout_ns) {
       spin_timeout(site, false);
     }
-    if (g_abort_flag != nullptr && *g_abort_flag != 0u) spin_timeout(site, true);
+    // the host abort word lives in pinned host memory: a PCIe read, so it is
+    // polled only by waits that already spun for > 1 ms (a straggling peer),
+    // never on the microsecond-scale waits of a healthy forward
+    if (t - t0 > 1000000ull && g_abort_flag != nullptr && *g_abort_flag != 0u) spin_timeout(site, true);
   }
 };
 

@@ -79,12 +79,17 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "matrix.jsonl"))
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--only", default="", help="comma list of SHAPE:EP:TP:M:STD (replaces the matrix)")
     ap.add_argument("--nc0", default="16,32,64", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
     a = ap.parse_args()
     burst, sust, hbm, src = load_peaks()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as fh:
-        for shape, ep, tp, M, std in configs(a.quick):
+        todo = configs(a.quick)
+        if a.only:
+            todo = [(f[0], int(f[1]), int(f[2]), int(f[3]), float(f[4])) for f in
+                    (c.split(":") for c in a.only.split(","))]
+        for shape, ep, tp, M, std in todo:
             E, topk, N, K = SHAPES[shape]
             model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
             par = ParallelSpec(tp=tp, ep=ep)
