@@ -313,12 +313,16 @@ def run_ours(args):
     routing = build_routing(model, par, WorkloadSpec(M=args.M, seed=0, std=args.std))
     M = args.M
     dev = torch.device("cuda", local)
-    # the dispatch CTAs must leave compute pairs: a reduced grid (COMET_GRID,
-    # the ranks-sharing-one-GPU test mode) caps them at half of it
-    grid = int(os.environ.get("COMET_GRID", torch.cuda.get_device_properties(local).multi_processor_count))
-    n_comm0 = max(2, min(args.n_comm0, (grid // 2) // 2 * 2))
-    knobs = LayerKnobs(n_comm0=n_comm0, n_comm1=args.n_comm1,
-                       group0=args.group0, wave1=args.wave1)
+    # n_comm0 None: the product path's adaptive chooser (measured split
+    # metadata, else the fitted cost model; MoELayer.split_choice).  The
+    # dispatch CTAs must leave compute pairs: a reduced grid (COMET_GRID, the
+    # ranks-sharing-one-GPU test mode) caps them at half of it.
+    grid_env = os.environ.get("COMET_GRID")
+    grid = int(grid_env) if grid_env else torch.cuda.get_device_properties(local).multi_processor_count
+    n_comm0 = None if args.n_comm0 is None else max(2, min(args.n_comm0, (grid // 2) // 2 * 2))
+    knobs = LayerKnobs.for_world(world, n_comm0=n_comm0, n_comm1=args.n_comm1, wave1=args.wave1,
+                                 grid=int(grid_env) if grid_env else None,
+                                 **({"group0": args.group0} if args.group0 is not None else {}))
     weights = rank_weights_random(model, par, rank, dev)
     layer = distributed.init_layer(model, par, M, weights, knobs=knobs) if world > 1 else \
         MoELayer(model, par, rank, M, weights, device=local, knobs=knobs)
@@ -473,7 +477,8 @@ def run_ours(args):
                              == "zerocopy" else "MoELayer.forward_host (H2D, forward, D2H)")},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
-            "knobs": {"n_comm0": knobs.n_comm0, "n_comm1": knobs.n_comm1, "group0": knobs.group0,
+            "knobs": {"n_comm0": layer.split_choice(M)[0], "n_comm0_source": layer.split_choice(M)[1],
+                      "n_comm1": knobs.n_comm1, "group0": knobs.group0,
                       "wave1": knobs.wave1},
         }
         if cpu is not None:
@@ -533,25 +538,18 @@ def main():
     ap.add_argument("--M", type=int, default=8192)
     ap.add_argument("--std", type=float, default=0.0)
     ap.add_argument("--n-comm0", type=int, default=None,
-                    help="layer0 dispatch CTAs (default 8 per rank of the group, max 64: measured best at EP=2/4/8)")
+                    help="layer0 dispatch CTAs (default: the adaptive chooser -- measured split metadata, "
+                         "else the fitted cost model)")
     ap.add_argument("--n-comm1", type=int, default=0)
     ap.add_argument("--group0", type=int, default=None,
-                    help="layer0 pair-group raster (default: 8 at EP=1 and EP>=8, 4 at EP=2/4; measured)")
+                    help="layer0 pair-group raster (default LayerKnobs.for_world: 8 at EP=1 and EP>=8, 4 at "
+                         "EP=2/4; measured)")
     ap.add_argument("--wave1", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.n_comm0 is None:
-        # measured (gpu_run106.sh, tools/matrix.py): EP=2 16 vs 64 CTAs
-        # 1.396 vs 1.409 ms, EP=4 32 vs 64 0.734 vs 0.742 ms, EP=8 64 best
-        args.n_comm0 = min(64, 8 * args.gpus)
-    if args.group0 is None:
-        # measured (tools/gpu_runs/gpu_run105.sh, 3 reps): 8-pair groups win at
-        # EP=1 and EP=8 (all 8 pairs of a rank in one group: 0.423 -> 0.417 ms),
-        # 4-pair groups at EP=2/4 (1.386 vs 1.404, 0.737 vs 0.744 ms)
-        args.group0 = 8 if args.gpus == 1 or args.gpus >= 8 else 4
     return run_reference(args) if args.impl == "reference" else run_ours(args)
 
 

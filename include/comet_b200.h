@@ -254,7 +254,11 @@ int comet_device_info(int device, int32_t out[4]);
  *   STREAM_FUSE    streamed host forward: epilogue fold instead of the
  *                  dispatch-CTA combine (0)
  *   SEQUENTIAL     no overlap: layer0 GEMMs start after the WHOLE dispatch
- *                  (the all-to-all-then-GroupGEMM baseline of the cli; 0) */
+ *                  (the all-to-all-then-GroupGEMM baseline of the cli; 0)
+ *   STREAMK        1: layer1's single partial round (pairs/2 < tiles < pairs,
+ *                  no fold chains) as head / tail K slices, the tails
+ *                  filling the idle pairs (sched.cuh; measured no faster
+ *                  than whole units at Mixtral EP=8 -- kept opt-in; 0) */
 #define COMET_OPT_FUSED 0
 #define COMET_OPT_KSPLIT_MAX 1
 #define COMET_OPT_SPLIT_TAIL0 2
@@ -275,7 +279,8 @@ int comet_device_info(int device, int32_t out[4]);
 #define COMET_OPT_ZC_FOLD_ORDER 17
 #define COMET_OPT_STREAM_FUSE 18
 #define COMET_OPT_SEQUENTIAL 19
-#define COMET_OPT_COUNT 20
+#define COMET_OPT_STREAMK 20
+#define COMET_OPT_COUNT 21
 #define COMET_OPT_DEFAULT (-2147483647 - 1)
 int comet_set_option(comet_ctx* ctx, int opt, int value);
 int comet_get_option(comet_ctx* ctx, int opt, int* value);

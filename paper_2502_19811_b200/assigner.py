@@ -169,65 +169,41 @@ def record_from_curve(key: SplitKey, points: Sequence[Tuple[int, int]]) -> Split
 def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSpec,
                 cost=None, cost_name: str = "b200", blocks: Optional[int] = None,
                 stride: int = 2, rank: int = 0, max_nc: int = 16, repeats: int = 5,
-                measure: Optional[Callable[[int], float]] = None) -> SplitRecord:
+                measure: Optional[Callable[[int], float]] = None,
+                candidates: Optional[Sequence[int]] = None) -> SplitRecord:
     """Measure the fused layer at each candidate n_c and record the argmin.
 
-    ``measure(n_c) -> seconds`` defaults to timing ``MoELayer`` on this GPU
-    with synthetic tokens and random weights of the model's shape (single
-    device; for world > 1 the ranks are emulated on the device, so the curve
-    reflects on-device comm traffic -- the multi-GPU sweep uses
-    bench.py --sweep under torchrun).  ``cost`` is accepted for signature
-    compatibility with the reference and ignored.
+    ``measure(n_c) -> seconds`` defaults to timing the layer on this GPU with
+    synthetic tokens and random weights of the model's shape, every rank of
+    ``parallel`` emulated on the device (``measure.EmulatedGroup``: latency =
+    max over ranks of the rank's kernel time, the other knobs at the product
+    defaults of ``LayerKnobs.for_world``).  ``candidates`` overrides the
+    even grid ``candidate_ncs(blocks, stride, max_nc)``.  ``cost`` is
+    accepted for signature compatibility with the reference and ignored.
     """
     if blocks is None:
         from . import _lib
         blocks = _lib.device_info(0)["sms"]
     if measure is None:
         measure = _default_measure(model, parallel, workload, repeats)
-    points = [(nc, int(round(measure(nc) * 1e9))) for nc in candidate_ncs(blocks, stride, max_nc)]
+    cands = list(candidates) if candidates is not None else candidate_ncs(blocks, stride, max_nc)
+    points = [(nc, int(round(measure(nc) * 1e9))) for nc in cands]
     key = SplitKey.for_config(model, parallel, workload.M, cost_name, blocks)
     return record_from_curve(key, points)
 
 
 def _default_measure(model, parallel, workload, repeats):
-    import numpy as np
-    from . import _lib
-    from .executor import LayerKnobs, RankWeights, MoELayer, _layers
+    import dataclasses
+    from .executor import LayerKnobs
+    from .measure import EmulatedGroup
     from .routing import build_routing
-    torch = _lib.require_device()
     routing = build_routing(model, parallel, workload)
-    g = torch.Generator(device="cuda").manual_seed(workload.seed + 2)
-    w0 = torch.randn(model.E, model.N, model.K, device="cuda", generator=g) / math.sqrt(model.N)
-    w1 = torch.randn(model.E, model.K, model.N, device="cuda", generator=g) / math.sqrt(model.N)
-    rws = [RankWeights.from_full(w0, w1, model, parallel, r) for r in range(parallel.world_size)]
-    del w0, w1
-    layers = _layers(model, parallel, max(1, workload.M), rws, 0)
-    x = torch.randn(workload.M, model.N, device="cuda", generator=g).to(torch.bfloat16)
-    ex = torch.from_numpy(routing.as_array().copy()).cuda()
-    outs = []
-    for layer in layers:
-        lo, hi = layer.token_range(workload.M)
-        layer.place_tokens(x[lo:hi], workload.M)
-        outs.append(torch.empty(hi - lo, layer.n_pad, dtype=torch.bfloat16, device="cuda"))
-
-    def run(nc):
-        for layer, y in zip(layers, outs):
-            layer.knobs = LayerKnobs(n_comm0=nc, n_comm1=nc)
-        from .executor import _phase_forward
-        _phase_forward(layers, ex, workload.M, outs, None)
+    grp = EmulatedGroup(model, parallel, routing, seed=workload.seed + 2)
+    base = LayerKnobs.for_world(parallel.world_size)
 
     def measure(nc):
-        run(nc)
-        torch.cuda.synchronize()
-        times = []
-        for _ in range(repeats):
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            run(nc)
-            e.record()
-            torch.cuda.synchronize()
-            times.append(s.elapsed_time(e) / 1e3)
-        return float(sorted(times)[len(times) // 2])
+        grp.set_knobs(dataclasses.replace(base, n_comm0=nc))
+        return grp.measure(iters=repeats)["latency_ms"] * 1e-3
     return measure
 
 
@@ -249,3 +225,38 @@ def select_split(metadata: SplitMetadata, query: SplitKey) -> KernelSplit:
             raise UnprofiledConfigError(f"cannot bucket a token count of {query.m}; profile it explicitly")
         chosen = min(compatible, key=lambda r: (abs(math.log2(query.m) - math.log2(r.key.m)), r.key.m))
     return split_for(chosen.key.blocks, chosen.optimal_nc)
+
+
+# ---------------------------------------------------------------------------
+# The product path's chooser (paper section 3.3: n_c from measured timings)
+# ---------------------------------------------------------------------------
+
+DEFAULT_METADATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "split_b200.json")
+_default_meta: Optional[SplitMetadata] = None
+
+
+def default_metadata() -> SplitMetadata:
+    """The committed n_c sweep measured on B200 (tools/sweep_b200.py ->
+    ``split_b200.json``, the reference's SplitMetadata schema, cost "b200")."""
+    global _default_meta
+    if _default_meta is None:
+        _default_meta = SplitMetadata.load(DEFAULT_METADATA) if os.path.exists(DEFAULT_METADATA) \
+            else SplitMetadata(records=[])
+    return _default_meta
+
+
+def choose_split(model: ModelConfig, parallel: ParallelSpec, m_tokens: int, blocks: int,
+                 metadata: Optional[SplitMetadata] = None) -> Tuple[KernelSplit, str]:
+    """Communication blocks n_c of the fused layer for ``m_tokens`` tokens, as
+    the reference's cli picks them (cli.py:228-235): ``select_split`` on the
+    measured metadata (exact key, else the nearest log2 token bucket,
+    assigner.py:260-292); for an unprofiled shape the fitted b200 cost model
+    (costmodel.predict_split) instead of ``UnprofiledConfigError``.  Returns
+    (split, "measured" | "model")."""
+    meta = metadata if metadata is not None else default_metadata()
+    try:
+        return select_split(meta, SplitKey.for_config(model, parallel, m_tokens, "b200", blocks)), "measured"
+    except UnprofiledConfigError:
+        from .costmodel import predict_split
+        rec = predict_split(model, parallel, WorkloadSpec(M=max(1, m_tokens), seed=0))
+        return split_for(blocks, min(rec.optimal_nc, blocks - 2)), "model"

@@ -73,7 +73,7 @@ constexpr int kOptDefaults[COMET_OPT_COUNT] = {
     /*FUSED*/ 1, /*KSPLIT_MAX*/ 8, /*SPLIT_TAIL0*/ 1, /*SPLIT1*/ -1, /*DEDUP*/ -1, /*PULL_LOCAL*/ 1,
     /*FOLD_ORDER*/ 1, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 6, /*GRID*/ 0, /*FUSE1*/ 0,
     /*SPIN_TIMEOUT_MS*/ 600000, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
-    /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0};
+    /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0, /*STREAMK*/ 0};
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous one drains; it calls griddepcontrol.wait before touching
@@ -686,8 +686,9 @@ static int ensure_work(comet_ctx* x) {
   CK(cudaMalloc(&x->h_cnt, sizeof(uint32_t) * x->n_h));
   CK(cudaMemset(x->h_cnt, 0, sizeof(uint32_t) * x->n_h));
   // split-K only runs when a layer's output tiles x slices <= pairs: each
-  // layer needs at most (grid/2 pairs) x 2 CTA tiles of 128 x 512 fp32
-  CK(cudaMalloc(&x->part, (size_t)2 * x->n_sm * kTileRows * kBlockN * sizeof(float)));
+  // layer needs at most (grid/2 pairs) x 2 CTA tiles of 128 x 512 fp32;
+  // layer1 also holds the stream-K tail's partials: two per range, ranges <= pairs
+  CK(cudaMalloc(&x->part, (size_t)3 * x->n_sm * kTileRows * kBlockN * sizeof(float)));
   CK(cudaMalloc(&x->split_cnt, sizeof(uint32_t) * 2 * 512));
   CK(cudaMemset(x->split_cnt, 0, sizeof(uint32_t) * 2 * 512));
   int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
@@ -837,6 +838,7 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   a.layer = 1;
   a.part = x->part + (size_t)x->n_sm * kTileRows * kBlockN;
   a.split_cnt = x->split_cnt + 512;
+  a.streamk = x->opt[COMET_OPT_STREAMK] != 0;
   a.n_blocks = x->nb1;
   a.k_blocks = x->kb1;
   a.b_rows = c.N;

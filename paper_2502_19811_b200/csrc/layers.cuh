@@ -41,6 +41,7 @@ struct LayerArgs {
   int split_tail;         // layer0 (alone): cut a mostly idle last round into 256-column half units
   int split_units;        // layer1: the last `split_units` full units run as 256-column halves
   int ksplit_max;         // split-K slices allowed when output tiles are fewer than pairs (0 = off)
+  int streamk;            // layer1: stream-K tail (sched.cuh) instead of whole units in the last round
   float* part;            // split-K fp32 partials [tiles*NB][S][128][512] (<= pairs*2 CTA tiles)
   uint32_t* split_cnt;    // [tiles*NB] slices landed (reset by the finisher)
   uint32_t epoch;

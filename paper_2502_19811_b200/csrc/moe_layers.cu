@@ -319,8 +319,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       }
       __syncwarp();
       const uint64_t t_start = ptx::globaltimer();  // load interval starts once its A rows are ready
-      const int S = slices_of(w, s0, s1);
-      const int kb0 = w.ks * p.k_blocks / S, kb1 = (w.ks + 1) * p.k_blocks / S;
+      const int kb0 = w.kb0, kb1 = w.kb1;
       const int kb_req = max(kb0, kb1 - kClaimLead);
       for (int kb = kb0; kb < kb1; ++kb) {
         wait(empty + stage, phase ^ 1);
@@ -355,8 +354,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const LayerArgs& p = f.l[w.layer];
       const bool two = w.half < 0;  // both accumulator halves (else only half 0)
       const uint32_t ephase = (it & 1) ^ 1;  // previous unit's drain of each half
-      const int S = slices_of(w, s0, s1);
-      const int kb0 = w.ks * p.k_blocks / S, kb1 = (w.ks + 1) * p.k_blocks / S;
+      const int kb0 = w.kb0, kb1 = w.kb1;
       const uint64_t t_w = ptx::globaltimer();
       wait(tempty + 0, ephase);
       ptx::tc_fence_after();
@@ -555,12 +553,44 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // split-K: this slice's fp32 partial of the CTA's 128 x 512 tile, stored
       // column-quad major ([c/4][row][4]) so a warp's 32 rows of one quad are
       // 512 contiguous bytes (coalesced stores and reloads)
-      const int S = slices_of(w, s0, s1);
+      // split-K: this slice's fp32 partial of the CTA's 128 x 512 tile, stored
+      // column-quad major ([c/4][row][4]) so a warp's 32 rows of one quad are
+      // 512 contiguous bytes (coalesced stores and reloads)
+      const int S = w.np;
       const long long split_tile = static_cast<long long>(row0 >> 7) * NB + w.nb;
       float4* part_row = S > 1 ? reinterpret_cast<float4*>(p.part + (split_tile * S + w.ks) * kTileRows * kBlockN) +
                                      ew * 32 + lane
                                : nullptr;
-      if (S == 1) fold_wait();
+      // Split-K finisher.  Two slices (the uneven layer1 tail split, or S = 2
+      // split-K): roles are decided when the accumulator is ready -- the
+      // slice that starts its epilogue last finishes the tile; the other
+      // stores its fp32 partial and counts it as landed; the finisher waits
+      // for it and drains its own accumulator adding the partial (0 + slice 0
+      // + slice 1: IEEE addition commutes, so the value is the same whichever
+      // slice finishes -- bitwise deterministic), so its own partial is never
+      // written and re-read.  More slices (small-M split-K): every slice
+      // stores its partial; the last to land sums all S in slice order after
+      // its accumulator is released.
+      const bool early = S == 2;
+      bool finisher = S == 1;  // this CTA produces the tile's output (always, without split-K)
+      uint32_t* landed = p.split_cnt + 256 + split_tile;
+      const float4* rows0 =
+          S > 1 ? reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + ew * 32 + lane : nullptr;
+      if (early) {
+        ptx::named_bar_sync(1, 128);
+        if (threadIdx.x == kEpiThread0) *sflag = atomicAdd(p.split_cnt + split_tile, 1u) == 1u;
+        ptx::named_bar_sync(1, 128);
+        finisher = *reinterpret_cast<volatile int*>(sflag) != 0;
+        if (finisher) {
+          if (threadIdx.x == kEpiThread0) {
+            ptx::Spin sp;
+            while (ptx::ld_acquire_gpu(landed) < 1u) sp.pause(64, 6);
+          }
+          ptx::named_bar_sync(1, 128);
+          __threadfence();
+        }
+      }
+      if (finisher) fold_wait();
 #pragma unroll 1
       for (int s = 0; s < n_chunks; ++s) {
         const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
@@ -577,6 +607,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           continue;
         }
         uint32_t v0[32], v1[32];
+        const bool red2 = early && finisher && s * 64 < cols_left;
         ptx::tmem_ld32(taddr + s * 64, v0);
         ptx::tmem_ld32(taddr + s * 64 + 32, v1);
         ptx::tmem_ld_wait();
@@ -592,7 +623,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
             else ptx::mbar_arrive_cluster(tempty + 1, 0);
           }
         }
-        if (S > 1) {
+        if (!finisher) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             part_row[(s * 16 + i) * kTileRows] = make_float4(__uint_as_float(v0[4 * i]), __uint_as_float(v0[4 * i + 1]),
@@ -604,16 +635,41 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           continue;
         }
         if (s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;
+        if (red2) {
+          // 0 + slice 0 + slice 1 in slice order (IEEE addition commutes:
+          // (0 + other) + own is that value whichever slice is this one)
+          const float4* src = rows0 + static_cast<long long>(w.ks ^ 1) * (kTileRows * kBlockN / 4) + s * 16 * kTileRows;
+#pragma unroll
+          for (int hv = 0; hv < 2; ++hv) {
+            uint32_t* v = hv ? v1 : v0;
+            float4 q[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) q[i] = __ldcg(src + (hv * 8 + i) * kTileRows);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              v[4 * i] = __float_as_uint((0.f + q[i].x) + __uint_as_float(v[4 * i]));
+              v[4 * i + 1] = __float_as_uint((0.f + q[i].y) + __uint_as_float(v[4 * i + 1]));
+              v[4 * i + 2] = __float_as_uint((0.f + q[i].z) + __uint_as_float(v[4 * i + 2]));
+              v[4 * i + 3] = __float_as_uint((0.f + q[i].w) + __uint_as_float(v[4 * i + 3]));
+            }
+          }
+        }
         process(s, v0, v1);
       }
       if (tma_out) {  // this warp's tensor stores complete before the unit is counted
         if (lane == 0) ptx::bulk_wait<0>();
         __syncwarp();
       }
-      bool finisher = true;  // this CTA produces the tile's output (always, without split-K)
-      if (S > 1) {
-        // the last slice to land reduces all S partials in slice order
-        // (deterministic) and runs the epilogue proper
+      if (early) {
+        if (!finisher) {  // partial in memory -> landed
+          __threadfence();
+          ptx::named_bar_sync(1, 128);
+          if (threadIdx.x == kEpiThread0) ptx::red_release_gpu_add(landed, 1u);
+        } else if (threadIdx.x == kEpiThread0) {  // both slices arrived and landed: reset for the next launch
+          p.split_cnt[split_tile] = 0u;
+          *landed = 0u;
+        }
+      } else if (S > 1) {
         __threadfence();
         ptx::named_bar_sync(1, 128);
         if (threadIdx.x == kEpiThread0) *sflag = atomicAdd(p.split_cnt + split_tile, 1u) == static_cast<uint32_t>(S - 1);
@@ -622,7 +678,6 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (finisher) {
           __threadfence();
           fold_wait();
-          const float4* rows0 = reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + ew * 32 + lane;
 #pragma unroll 1
           for (int s = 0; s < n_chunks; ++s) {
             if (s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;

@@ -153,7 +153,7 @@ class LayerKnobs:
     keeps the library's measured default.  Nothing is read from the
     environment."""
 
-    n_comm0: int = 64
+    n_comm0: Optional[int] = None  # None: the adaptive chooser (assigner.choose_split) per token count
     n_comm1: int = 0
     group0: int = 4
     wave1: int = 4
@@ -180,13 +180,15 @@ class LayerKnobs:
     zc_fold_order: Optional[bool] = None
     stream_fuse: Optional[bool] = None
     sequential: Optional[bool] = None
+    streamk: Optional[bool] = None
 
     @classmethod
     def for_world(cls, world: int, **options) -> "LayerKnobs":
-        """Measured defaults (bench.py): 8 dispatch CTAs per rank
-        of the group (max 64); 8-pair layer0 groups at EP=1 and EP>=8, 4-pair
-        groups at EP=2/4."""
-        return cls(n_comm0=min(64, 8 * max(1, world)), group0=8 if world == 1 or world >= 8 else 4, **options)
+        """Measured defaults: n_comm0 left to the adaptive
+        chooser (measured split metadata, else the fitted cost model);
+        8-pair layer0 groups at EP=1 and EP>=8, 4-pair groups at EP=2/4."""
+        options.setdefault("group0", 8 if world == 1 or world >= 8 else 4)
+        return cls(**options)
 
     def options(self) -> Dict[str, Optional[int]]:
         """The COMET_OPT_* values (None = library default)."""
@@ -225,6 +227,30 @@ class MoELayer:
         self.knobs = knobs or LayerKnobs.for_world(parallel.world_size)
         self.device = device
         self._xbuf = self.ctx.token_buffer()
+        self._nc_cache: Dict[int, tuple] = {}
+
+    def n_comm0(self, M: int) -> int:
+        """Layer0 dispatch CTAs for a forward of M tokens: 0 at world 1 (no
+        remote rows), the knob when set, else the adaptive chooser's n_c
+        (``assigner.choose_split``: measured sweep, else the fitted cost
+        model), cached per M."""
+        return self.split_choice(M)[0]
+
+    def split_choice(self, M: int):
+        """(n_comm0, source) -- source "knob", "measured", "model" or "world1"."""
+        if self.parallel.world_size == 1:
+            return 0, "world1"
+        if self.knobs.n_comm0 is not None:
+            return self.knobs.n_comm0, "knob"
+        hit = self._nc_cache.get(M)
+        if hit is None:
+            from .assigner import choose_split
+            blocks = self.knobs.grid or _lib.device_info(self.device)["sms"]
+            split, src = choose_split(self.model, self.parallel, M, blocks)
+            # the kernel needs an even count leaving >= one compute pair
+            nc = max(2, min(split.n_c, (blocks // 2) // 2 * 2) // 2 * 2)
+            hit = self._nc_cache[M] = (nc, src)
+        return hit
 
     @property
     def knobs(self) -> LayerKnobs:
@@ -272,7 +298,7 @@ class MoELayer:
         k = self.knobs
         world = self.parallel.world_size
         self.ctx.forward(experts, M, self.weights.w0t, self.weights.w1t, combine_w, y_local,
-                         activation=self.act, n_comm0=k.n_comm0 if world > 1 else 0,
+                         activation=self.act, n_comm0=self.n_comm0(M),
                          n_comm1=self.n_comm1(),
                          group0=k.group0, wave1=k.wave1, stream=stream)
 
@@ -592,11 +618,11 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
         for layer, y in zip(layers, outs):
             k = layer.knobs
             layer.ctx.layers(layer.weights.w0t, layer.weights.w1t, cw, y, layer.act,
-                             k.n_comm0 if world > 1 else 0, k.group0, k.wave1, stream=stream)
+                             layer.n_comm0(M), k.group0, k.wave1, stream=stream)
     else:
         for layer in layers:
             k = layer.knobs
-            layer.ctx.layer0(layer.weights.w0t, layer.act, k.n_comm0 if world > 1 else 0, k.group0, stream=stream)
+            layer.ctx.layer0(layer.weights.w0t, layer.act, layer.n_comm0(M), k.group0, stream=stream)
         for layer, y in zip(layers, outs):
             k = layer.knobs
             layer.ctx.layer1(layer.weights.w1t, cw, y, layer.n_comm1(), k.wave1,

@@ -6,9 +6,14 @@
 //   (2) put every layer0 unit of a pair before any layer1 unit of that pair
 //       (a layer1 unit waits for its H rows; an earlier claim never waits on
 //       a later one, so the persistent grid cannot deadlock);
-//   (3) keep, for each layer1 n-block, pairs in ascending order (the fused
-//       combine's fold reads rows of earlier pairs at the same columns).
+//   (3) keep, for each layer1 n-block, pairs in ascending order when the
+//       fused combine has fold chains (a token's last hosted row reads rows
+//       of earlier pairs at the same columns);
+//   (4) give the K slices of a split tile contraction ranges [kb0, kb1)
+//       that partition [0, KB) (even split-K and the uneven head / tail split
+//       of layer1's partial round).
 // Prints "OK <cases>" or the first violation.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -24,6 +29,7 @@ static int check(const KernelArgs& f, int P, int n_pairs, const char* tag) {
   Sched s0, s1;
   const int total = seq_total(f, P, n_pairs, s0, s1);
   std::map<std::tuple<int, int, int>, std::vector<std::pair<int, int>>> seen;  // (layer,pair,nb) -> (half,ks)
+  std::map<std::tuple<int, int, int>, std::vector<std::pair<int, int>>> kr;    // -> (kb0, kb1) per slice
   std::vector<int> l0_last(P, -1), l1_first(P, 1 << 30);
   std::map<int, int> last_pair_at_nb;  // layer1: nb*2+half -> last pair seen
   for (int g = 0; g < total; ++g) {
@@ -33,6 +39,11 @@ static int check(const KernelArgs& f, int P, int n_pairs, const char* tag) {
       return 1;
     }
     seen[{w.layer, w.pair, w.nb}].push_back({w.half, w.ks});
+    kr[{w.layer, w.pair, w.nb}].push_back({w.kb0, w.kb1});
+    if (w.np != (w.layer ? s1.S : s0.S)) {
+      printf("FAIL %s: g=%d slice count %d != S\n", tag, g, w.np);
+      return 1;
+    }
     if (w.layer == 0) l0_last[w.pair] = g;
     else {
       if (g < l1_first[w.pair]) l1_first[w.pair] = g;
@@ -40,7 +51,7 @@ static int check(const KernelArgs& f, int P, int n_pairs, const char* tag) {
         if (w.half >= 0 && w.half != h) continue;
         const int key = w.nb * 2 + h;
         auto it = last_pair_at_nb.find(key);
-        if (it != last_pair_at_nb.end() && it->second > w.pair) {
+        if (it != last_pair_at_nb.end() && it->second > w.pair && fold_chains(f.l[1])) {
           printf("FAIL %s: layer1 nb %d half %d visits pair %d after pair %d (g=%d)\n", tag, w.nb, h, w.pair,
                  it->second, g);
           return 1;
@@ -76,6 +87,20 @@ static int check(const KernelArgs& f, int P, int n_pairs, const char* tag) {
         if (!ok) {
           printf("FAIL %s: layer %d pair %d nb %d claimed %zu times (bad halves/slices)\n", tag, layer, pr, nb,
                  v.size());
+          return 1;
+        }
+        std::vector<std::pair<int, int>> r = kr[{layer, pr, nb}];
+        std::sort(r.begin(), r.end());
+        const int KB = f.l[layer].k_blocks;
+        bool kok = true;
+        if (s.S > 1) {
+          kok = r.front().first == 0 && r.back().second == KB;
+          for (size_t i = 0; i < r.size() && kok; ++i) kok = r[i].second > r[i].first && (i == 0 || r[i].first == r[i - 1].second);
+        } else {
+          for (auto& e : r) kok = kok && e.first == 0 && e.second == KB;
+        }
+        if (!kok) {
+          printf("FAIL %s: layer %d pair %d nb %d K slices do not partition [0, %d)\n", tag, layer, pr, nb, KB);
           return 1;
         }
       }
@@ -119,11 +144,15 @@ int main(int argc, char** argv) {
       a.ksplit_max = pick(0, 1) ? 8 : 0;
       b.ksplit_max = pick(0, 1) ? 8 : 0;
       b.split_units = std::vector<int>{0, 0, 5, 55, 74, 1000}[pick(0, 5)];
+      b.streamk = pick(0, 2) != 0;
+      b.fuse_combine = pick(0, 1);
+      b.experts_per_group = pick(1, 8);
+      b.topk = pick(1, 8);
     }
     char tag[160];
-    snprintf(tag, sizeof tag, "case %d (P=%d pairs=%d NB0=%d NB1=%d G=%d G2=%d ilv=%d split0=%d split1=%d ks=%d/%d)", c, P,
-             n_pairs, a.n_blocks, b.n_blocks, a.order_group, b.order_group2, f.interleave, a.split_tail,
-             b.split_units, a.ksplit_max, b.ksplit_max);
+    snprintf(tag, sizeof tag, "case %d (P=%d pairs=%d NB0=%d NB1=%d KB1=%d G=%d G2=%d ilv=%d split0=%d split1=%d ks=%d/%d sk=%d)", c,
+             P, n_pairs, a.n_blocks, b.n_blocks, b.k_blocks, a.order_group, b.order_group2, f.interleave,
+             a.split_tail, b.split_units, a.ksplit_max, b.ksplit_max, b.streamk);
     if (check(f, P, n_pairs, tag)) return 1;
   }
   printf("OK %d\n", n_cases);

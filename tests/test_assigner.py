@@ -58,3 +58,29 @@ def test_select_exact_then_nearest_log2_bucket(tmp_path):
 def test_candidates_even_cluster_multiples():
     assert candidate_ncs(148, 2, 12) == [2, 4, 6, 8, 10, 12]
     assert all(nc % 2 == 0 for nc in candidate_ncs(148, 3, 40))
+
+
+def test_product_chooser_uses_measured_metadata_then_cost_model():
+    """The layer's n_c (MoELayer.split_choice -> assigner.choose_split) is the
+    committed B200 sweep's select_split answer for profiled shapes (exact
+    key, else nearest log2 bucket) and the fitted cost model's
+    predict_split answer for unprofiled ones (ref cli.py:228-235)."""
+    from paper_2502_19811_b200 import costmodel
+    from paper_2502_19811_b200.assigner import choose_split, default_metadata
+    meta = default_metadata()
+    assert meta.records, "split_b200.json (tools/sweep_b200.py) must be committed"
+    par = ParallelSpec(1, 8)
+    for m in (8192, 6000, 50000):
+        split, src = choose_split(MX, par, m, 148)
+        assert src == "measured"
+        assert split == select_split(meta, key(m))
+        assert split.n == 148 and split.n_c % 2 == 0
+    # every committed record is the argmin of its own measured curve
+    for r in meta.records:
+        assert r.key.cost == "b200" and r.key.blocks == 148
+        assert (r.optimal_nc, r.latency_ns) == min(r.curve, key=lambda pt: (pt[1], pt[0]))
+    # unprofiled shape (an embed no sweep covered): the cost model answers
+    odd = ModelConfig(L=1, E=8, topk=2, N=2048, K=8192)
+    split, src = choose_split(odd, ParallelSpec(1, 4), 4096, 148)
+    assert src == "model"
+    assert split.n_c == costmodel.predict_split(odd, ParallelSpec(1, 4), WorkloadSpec(M=4096, seed=0)).optimal_nc

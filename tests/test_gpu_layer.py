@@ -207,6 +207,30 @@ def test_launch_modes_bitwise_equal(tp, ep, topk, std):
     assert_close(outs[0], ref, what=f"modes tp={tp} ep={ep} topk={topk}")
 
 
+@pytest.mark.parametrize("ep,M", [(1, 6000), (8, 49152)])
+def test_streamk_tail_split(ep, M):
+    """COMET_OPT_STREAMK: layer1's single partial round (pairs/2 < tiles <
+    pairs, no fold chains) as uneven head / tail K slices, the finisher
+    decided at epilogue start and adding the other slice's partial while it
+    drains (sched.cuh, moe_layers.cu).  Against the oracle, and run-to-run
+    bitwise (the two-slice sum is order-fixed whichever slice finishes)."""
+    model = ModelConfig(L=1, E=8, topk=2, N=512, K=1024)
+    par = ParallelSpec(1, ep)
+    routing = build_routing(model, par, WorkloadSpec(M=M, seed=51, std=0.0))
+    # tiles of layer1 on each rank (N = 512: one n-block) = its 256-row pairs
+    counts = np.asarray(routing.expert_counts).reshape(ep, -1)
+    tiles = [int(sum((c + 255) // 256 for c in row)) for row in counts]
+    assert all(37 < t < 73 for t in tiles), tiles
+    w = random_weights(model, seed=52)
+    x = np.random.default_rng(53).standard_normal((M, 512))
+    outs = [run_emulated(x, w, routing, par, knobs=LayerKnobs(n_comm0=4 if ep > 1 else 0, n_comm1=0, streamk=sk))
+            .cpu().numpy() for sk in (True, True, False)]
+    np.testing.assert_array_equal(outs[0], outs[1])
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array())
+    assert_close(outs[0], ref, what=f"streamk ep={ep}")
+    assert_close(outs[2], ref, what=f"whole units ep={ep}")
+
+
 @pytest.mark.parametrize("chunks", [1, 3, None, [512, 2000, 2000, 488]])
 def test_forward_host_pipeline(chunks):
     """Host-buffer end-to-end form: chunked H2D / forward / D2H pipeline

@@ -100,3 +100,31 @@ def test_measured_split_sweep_and_select(tmp_path):
     split = select_split(SplitMetadata.load(str(tmp_path / "split.json")),
                          SplitKey.for_config(model, ParallelSpec(1, 2), 2048, "b200", rec.key.blocks))
     assert split.n_c == rec.optimal_nc and split.n == rec.key.blocks
+
+
+def test_layer_takes_n_c_from_the_chooser():
+    """The product path (MoELayer with default knobs) launches with the n_c
+    the adaptive chooser picks: the committed measured sweep for a profiled
+    Mixtral EP=8 shape, the fitted cost model for an unprofiled one; an
+    explicit knob overrides both; world 1 has no dispatch CTAs."""
+    import torch
+    from paper_2502_19811_b200 import MoELayer, RankWeights, _lib
+    from paper_2502_19811_b200.assigner import choose_split
+    sms = _lib.device_info(0)["sms"]
+    for model, par, M, src in ((ModelConfig(L=1, E=8, topk=2, N=4096, K=14336), ParallelSpec(1, 8), 8192, "measured"),
+                               (ModelConfig(L=1, E=8, topk=2, N=512, K=1024), ParallelSpec(1, 2), 1000, "model")):
+        kl = model.K // par.tp
+        w = RankWeights(torch.zeros(model.E // par.ep, kl, model.N, dtype=torch.bfloat16, device="cuda"),
+                        torch.zeros(model.E // par.ep, model.N, kl, dtype=torch.bfloat16, device="cuda"))
+        layer = MoELayer(model, par, 0, M, w)
+        nc, got_src = layer.split_choice(M)
+        assert got_src == src
+        assert nc == choose_split(model, par, M, sms)[0].n_c
+        layer.knobs = LayerKnobs.for_world(par.world_size, n_comm0=6)
+        assert layer.split_choice(M) == (6, "knob")
+        layer.close()
+    w1 = RankWeights(torch.zeros(8, 1024, 512, dtype=torch.bfloat16, device="cuda"),
+                     torch.zeros(8, 512, 1024, dtype=torch.bfloat16, device="cuda"))
+    l1 = MoELayer(ModelConfig(L=1, E=8, topk=2, N=512, K=1024), ParallelSpec(), 0, 100, w1)
+    assert l1.split_choice(100) == (0, "world1")
+    l1.close()

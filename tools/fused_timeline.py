@@ -26,12 +26,14 @@ ap.add_argument("--nc0", type=int, default=8)
 ap.add_argument("--g0", type=int, default=4)
 ap.add_argument("--wave1", type=int, default=4)
 ap.add_argument("--pairs", type=int, default=8, help="pairs to print in detail")
+ap.add_argument("--knobs", default="", help="extra LayerKnobs fields, e.g. streamk=0")
 a = ap.parse_args()
 E, topk, N, K = SHAPES[a.shape]
 model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
 par = ParallelSpec(a.tp, a.ep)
 routing = build_routing(model, par, WorkloadSpec(M=a.M, seed=0, std=a.std))
-grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=a.nc0, n_comm1=0, group0=a.g0, wave1=a.wave1))
+extra = {k: int(v) for k, v in (kv.split("=") for kv in a.knobs.split(",") if kv)}
+grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=a.nc0, n_comm1=0, group0=a.g0, wave1=a.wave1, **extra))
 r = grp.measure(iters=5)
 print("measured:", {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items() if k != "per_rank_ms"})
 l0 = grp.layers[0]
@@ -72,6 +74,12 @@ for k in ("L0", "L1", "L1h"):
     d = [x[3] - x[2] for x in mma if kind(x[1]) == k]
     if d:
         print(f"  MMA {k:3s}: n={len(d):4d} mean {statistics.mean(d)/1e3:7.2f} us  min {min(d)/1e3:7.2f}  max {max(d)/1e3:7.2f}")
+    d = [x[3] - x[2] for x in by_role.get("tmem_wait", []) if kind(x[1]) == k]
+    if d:
+        print(f"  TMW {k:3s}: n={len(d):4d} mean {statistics.mean(d)/1e3:7.2f} us  max {max(d)/1e3:7.2f}")
+    d = [x[3] - x[2] for x in by_role.get("load", []) if kind(x[1]) == k]
+    if d:
+        print(f"  LD  {k:3s}: n={len(d):4d} mean {statistics.mean(d)/1e3:7.2f} us  max {max(d)/1e3:7.2f}")
     d = [(x[3] - x[2], x[3]) for x in by_role.get("epilogue", []) if kind(x[1]) == k]
     if d:
         print(f"  EPI {k:3s}: n={len(d):4d} mean {statistics.mean(v for v, _ in d)/1e3:7.2f} us  max {max(v for v, _ in d)/1e3:7.2f}"
@@ -90,6 +98,10 @@ for c in sorted(pairs):
         line = " ".join(f"{kind(t)}#{t}[{s/1e3:.0f}-{e/1e3:.0f}|ld{loads.get((c, t), (0, 0))[0]/1e3:.0f}]" for s, e, t in xs)
         print(f"  cta {c:3d}: units {len(xs):2d} busy {busy/1e3:6.1f} us | {line}")
 ends.sort()
+for e, c in ends[-4:]:
+    xs = sorted(pairs[c])
+    print(f"  late cta {c:3d}: " + " ".join(f"{kind(t)}[{s/1e3:.0f}-{e2/1e3:.0f}|ld{loads.get((c, t), (0, 0))[0]/1e3:.0f}]"
+                                            for s, e2, t in xs))
 print("pair end times (us): min %.1f median %.1f max %.1f" % (ends[0][0] / 1e3, ends[len(ends) // 2][0] / 1e3,
                                                             ends[-1][0] / 1e3))
 if life:

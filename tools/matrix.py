@@ -79,6 +79,8 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "matrix.jsonl"))
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--knobs", default="", help="extra LayerKnobs fields, e.g. streamk=0,split1=16")
+    ap.add_argument("--reps", type=int, default=1, help="measure each config this many times (best kept)")
     ap.add_argument("--only", default="", help="comma list of SHAPE:EP:TP:M:STD (replaces the matrix)")
     ap.add_argument("--nc0", default="16,32,64", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
     a = ap.parse_args()
@@ -96,15 +98,16 @@ def main():
             routing = build_routing(model, par, WorkloadSpec(M=M, seed=0, std=std))
             rf_b, rf_s = roofline(routing, burst), roofline(routing, sust)
             t0 = time.time()
-            grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=2, n_comm1=0))
+            extra = {k: int(v) for k, v in (kv.split("=") for kv in a.knobs.split(",") if kv)}
+            grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=2, n_comm1=0, **extra))
             best = None
-            for nc0 in ([0] if par.world_size == 1 else [int(v) for v in a.nc0.split(",")]):
-                grp.set_knobs(LayerKnobs(n_comm0=nc0, n_comm1=0))
+            for nc0 in ([0] if par.world_size == 1 else [int(v) for v in a.nc0.split(",")]) * a.reps:
+                grp.set_knobs(LayerKnobs(n_comm0=nc0, n_comm1=0, **extra))
                 r = grp.measure(iters=a.iters)
                 r["n_comm0"] = nc0
                 if best is None or r["latency_ms"] < best["latency_ms"]:
                     best = r
-            rec = {"shape": shape, "E": E, "topk": topk, "N": N, "K": K, "ep": ep, "tp": tp, "M": M, "std": std,
+            rec = {"knobs": a.knobs, "shape": shape, "E": E, "topk": topk, "N": N, "K": K, "ep": ep, "tp": tp, "M": M, "std": std,
                    "emulated": par.world_size > 1, "latency_ms": round(best["latency_ms"], 4),
                    "hot_rank": best["hot_rank"], "n_comm0": best["n_comm0"],
                    "kernels_ms_hot_rank": {k: round(v, 4) for k, v in best["kernels_ms_hot_rank"].items()},
