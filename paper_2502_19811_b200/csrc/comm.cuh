@@ -18,7 +18,10 @@ constexpr int kMaxSlots = 224;
 constexpr int kReducers = 7;               // combine: warps 1..7
 constexpr int kBatch = 16;                 // jobs described per loader pass
 constexpr uint32_t kRingBytes = 192 * 1024;
-constexpr int kFreeLag = 2;                // dispatch: bulk-store groups before a slot is reused
+#ifndef COMET_FREE_LAG
+#define COMET_FREE_LAG 2
+#endif
+constexpr int kFreeLag = COMET_FREE_LAG;   // dispatch: bulk-store groups in flight before a slot is reused
 constexpr int kPubLag = 24;                // dispatch: groups in flight before a tile is published
 constexpr int kJobSlots = 64;              // dedup dispatch ring slots (job descriptions in smem)
 constexpr int kPubBatch = 8;               // dedup dispatch: completed jobs counted per publication pass

@@ -1,7 +1,7 @@
 """Worker for tests/test_gpu_multiproc.py (torchrun, one process per rank).
 
 Every rank runs its own MoELayer (own CUDA context, own symmetric heap), the
-IPC handles are exchanged over gloo, and three consecutive forwards run
+IPC handles are exchanged over gloo (NCCL on distinct GPUs), and three consecutive forwards run
 concurrently across the processes -- the real multi-rank protocol (IPC-mapped
 peer heaps, system-scope epoch flags, dispatch pulls / combine pushes).  With
 COMET_SAME_DEVICE=1 all ranks share GPU 0 (LayerKnobs.grid splits the SMs so the
@@ -23,7 +23,12 @@ from paper_2502_19811_b200 import (LayerKnobs, ModelConfig, ParallelSpec, RankWe
 
 def main():
     tp, ep, topk = (int(v) for v in sys.argv[1:4])
-    dist.init_process_group("gloo")
+    backend = os.environ.get("COMET_TEST_BACKEND", "gloo")
+    if backend == "nccl":  # distinct GPUs: NCCL bootstrap, as bench.py / deployments use
+        torch.cuda.set_device(distributed.local_device())
+        dist.init_process_group("nccl", device_id=torch.device("cuda", distributed.local_device()))
+    else:
+        dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     model = ModelConfig(L=1, E=8, topk=topk, N=512, K=1024)
     par = ParallelSpec(tp, ep)
