@@ -36,6 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-gencode", "arch=compute_100a,code=sm_100a",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            "-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
+    # developer A/B builds only (compile-time experiment macros, e.g. -DCOMET_PUB_LAG=8)
+    cmd[1:1] = os.environ.get("COMET_NVCC_EXTRA", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

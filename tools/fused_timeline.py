@@ -119,3 +119,15 @@ comm = by_role.get("comm", [])
 if comm:
     print(f"  dispatch: {len(comm)} tiles, last published +{max(x[3] for x in comm)/1e3:.1f} us")
 grp.close()
+if comm and os.environ.get("DISP"):
+    # dispatch CTAs: items (storer start -> tile publication) per CTA
+    per = {}
+    for c, task, s, e in comm:
+        per.setdefault(c, []).append((s, e, task))
+    starts = sorted(min(x[0] for x in v) for v in per.values())
+    ends = sorted(max(x[1] for x in v) for v in per.values())
+    print(f"  dispatch CTAs {len(per)}: first item start min {starts[0]/1e3:.1f} max {starts[-1]/1e3:.1f} us;"
+          f" last publication min {ends[0]/1e3:.1f} median {ends[len(ends)//2]/1e3:.1f} max {ends[-1]/1e3:.1f} us")
+    for c in sorted(per)[:4] + sorted(per)[-4:]:
+        xs = sorted(per[c])
+        print(f"   cta {c:3d}: " + " ".join(f"q{t}[{s/1e3:.1f}-{e/1e3:.1f}]" for s, e, t in xs[:10]))
