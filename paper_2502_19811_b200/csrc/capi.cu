@@ -180,7 +180,7 @@ struct comet_ctx {
   const float* last_combine_w = nullptr;
   MapCache w0c, w1c;
   uint32_t* sched = nullptr;  // [2] unit claim / CTA exit counters of the layer kernel (self-resetting)
-  uint32_t* h_cnt = nullptr;  // [cap_rows_pad / 128 + 1] fused-launch H tile counters (self-resetting)
+  uint32_t* h_cnt = nullptr;  // [(cap_rows_pad / 128 + 1) * nb0] fused-launch H half counts (self-resetting)
   // host-streamed forward: upload / download streams, per-chunk upload epochs
   cudaStream_t up_stream = nullptr, down_stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_index = nullptr, ev_down = nullptr;
@@ -680,7 +680,7 @@ static int ensure_work(comet_ctx* x) {
   const size_t td = sizeof(uint32_t) * (x->cap_rows_pad / kTileRows + 1) * x->nb1 * 2;
   CK(cudaMalloc(&x->tile_done, td));
   CK(cudaMemset(x->tile_done, 0, td));
-  x->n_h = x->cap_rows_pad / kTileRows + 1;
+  x->n_h = (x->cap_rows_pad / kTileRows + 1) * x->nb0;  // per (128-row H tile, layer0 n-block)
   CK(cudaMalloc(&x->sched, sizeof(uint32_t) * 2));
   CK(cudaMemset(x->sched, 0, sizeof(uint32_t) * 2));
   CK(cudaMalloc(&x->h_cnt, sizeof(uint32_t) * x->n_h));

@@ -126,7 +126,7 @@ struct KernelArgs {
   int n_dl;          // mode 2: the first n_dl dispatch CTAs then download final output rows to y_host
   __nv_bfloat16* y_host;  // zero-copy forward: [M, N] pinned host output (l[1].y_local is the device copy)
   uint32_t* sched;   // [0] unit claim counter, [1] CTA exit counter (both reset by the last CTA)
-  uint32_t* h_cnt;   // [n_h] mode 2: layer0 half-units completed per 128-row H tile (reset at exit)
+  uint32_t* h_cnt;   // [n_h] mode 2: layer0 256-column halves landed per (128-row H tile, n-block) (reset at exit)
   int n_h;
 };
 

@@ -309,21 +309,28 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
           { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) sp.pause(32, 3); }
           ptx::fence_async_global();
-        } else if (w.layer == 1 && f.mode == 2) {
-          // layer1 A = H rows written by the layer0 epilogues of this launch
-          const uint32_t* hc = f.h_cnt + (row0 >> 7);
-          const uint32_t target = tile_halves(f.l[0]);
-          { ptx::Spin sp; while (ptx::ld_acquire_gpu(hc) < target) sp.pause(32, 4); }
-          ptx::fence_async_global();
         }
       }
       __syncwarp();
+      // layer1 A = H rows written by the layer0 epilogues of this launch:
+      // each 64-wide k-block is gated on the layer0 unit of its columns
+      // (per (128-row tile, layer0 n-block) half counts), so a layer1 unit
+      // starts as soon as its first H columns exist and reaches the columns
+      // of layer0's last units (the leftover round) ~a unit time later
+      const bool gate_h = w.layer == 1 && f.mode == 2;
+      const uint32_t* hc = f.h_cnt + static_cast<long long>(row0 >> 7) * f.l[0].n_blocks;
       const uint64_t t_start = ptx::globaltimer();  // load interval starts once its A rows are ready
       const int kb0 = w.kb0, kb1 = w.kb1;
       const int kb_req = max(kb0, kb1 - kClaimLead);
       for (int kb = kb0; kb < kb1; ++kb) {
         wait(empty + stage, phase ^ 1);
         if (kb == kb_req && leader && lane == 0) ptx::mbar_arrive(sreq);  // claim the next unit now
+        if (gate_h && lane == 0 && (kb == kb0 || (kb & (kBlockN / kBlockK - 1)) == 0)) {
+          const int nb0 = kb / static_cast<int>(kBlockN / kBlockK);
+          const uint32_t target = narrow_block(f.l[0], nb0) ? 1u : 2u;
+          { ptx::Spin sp; while (ptx::ld_acquire_gpu(hc + nb0) < target) sp.pause(32, 4); }
+          ptx::fence_async_global();
+        }
         if (lane == 0 && COMET_DBG(p.debug, 16)) {
           // debug: no data movement, complete the stage by arrivals only
           if (leader) ptx::mbar_arrive(full + stage);
@@ -717,7 +724,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         ptx::named_bar_sync(1, 128);
         if (threadIdx.x == kEpiThread0 && amount) {
           __threadfence();
-          ptx::red_release_gpu_add(f.h_cnt + (row0 >> 7), amount);
+          ptx::red_release_gpu_add(f.h_cnt + static_cast<long long>(row0 >> 7) * NB + w.nb, amount);
         }
       } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them

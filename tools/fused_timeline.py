@@ -131,3 +131,21 @@ if comm and os.environ.get("DISP"):
     for c in sorted(per)[:4] + sorted(per)[-4:]:
         xs = sorted(per[c])
         print(f"   cta {c:3d}: " + " ".join(f"q{t}[{s/1e3:.1f}-{e/1e3:.1f}]" for s, e, t in xs[:10]))
+if os.environ.get("GAPS"):
+    # per pair: MMA busy, gaps before each unit (claim / operand / TMEM waits)
+    tmw = {(c, t): (s, e) for c, t, s, e in by_role.get("tmem_wait", [])}
+    tot_busy = tot_gap = tot_head = tot_tail = 0.0
+    span_end = max(e for xs in pairs.values() for _, e, _ in xs)
+    for c in sorted(pairs):
+        xs = sorted(pairs[c])
+        busy = sum(e - s for s, e, _ in xs)
+        gaps = sum(xs[i + 1][0] - xs[i][1] for i in range(len(xs) - 1))
+        tot_busy += busy; tot_gap += gaps; tot_head += xs[0][0]; tot_tail += span_end - xs[-1][1]
+    n = len(pairs)
+    print(f"  pairs {n}: mean busy {tot_busy/n/1e3:.1f} us, gaps {tot_gap/n/1e3:.1f}, head {tot_head/n/1e3:.1f}, "
+          f"tail to last MMA end {tot_tail/n/1e3:.1f} (span to last MMA end {span_end/1e3:.1f})")
+    # MMA intervals include in-loop waits: operand (load) waits show as load start after claim
+    for k in ("L0", "L1", "L1h"):
+        d = [loads[(c, t)][0] - s for c, xs in pairs.items() for s, e, t in xs if kind(t) == k and (c, t) in loads]
+        if d:
+            print(f"  {k}: first load after MMA-start mean {statistics.mean(d)/1e3:.2f} us max {max(d)/1e3:.2f}")
