@@ -47,7 +47,8 @@ struct LayerArgs {
   uint32_t epoch;
   int debug;              // timing-experiment bits, compiled in only with -DCOMET_TIMING_EXPERIMENTS
                           // (COMET_DBG; wrong results unless noted): 1: comm CTAs idle; 4: spin
-                          // waits; 8: no MMA; 16: no loads; 64/128: no stores / no drain; 16384:
+                          // waits; 8: no MMA; 16: no loads; 64/128: no stores / no drain; 256: staged
+                          // in smem, not stored; 512: packed only; 16384:
                           // st.global epilogue instead of TMA stores (correct)
   int sequential;         // layer0: GEMMs start after the WHOLE dispatch (COMET_OPT_SEQUENTIAL; the
                           // no-overlap baseline of the cli, correct results)

@@ -528,10 +528,15 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           if (lane == 0) ptx::bulk_wait_read<1>();
           __syncwarp();
         }
+        if (COMET_DBG(p.debug, 512)) {  // debug: pack only (no staging, no stores)
+          if (pk[0] == 0x7fc07fc1u) p.split_cnt[0] = pk[1];  // keep the pack live
+          return;
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) * 16)) =
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        if (COMET_DBG(p.debug, 256)) return;  // debug: staged, not stored
         if (tma_out) {
           // rows row0+32*ew.. are contiguous in H / yrows: one async 2D tensor
           // store of the warp's 32 x 64 block (the swizzled staging layout is
