@@ -82,7 +82,9 @@ def main():
     ap.add_argument("--knobs", default="", help="extra LayerKnobs fields, e.g. streamk=0,split1=16")
     ap.add_argument("--reps", type=int, default=1, help="measure each config this many times (best kept)")
     ap.add_argument("--only", default="", help="comma list of SHAPE:EP:TP:M:STD (replaces the matrix)")
-    ap.add_argument("--nc0", default="16,32,64", help="layer0 comm-CTA counts tried for EP>1 (best kept)")
+    ap.add_argument("--nc0", default="auto",
+                    help="layer0 comm-CTA counts tried for EP>1 (best kept); 'auto' = the product chooser "
+                         "(assigner.choose_split on split_b200.json)")
     a = ap.parse_args()
     burst, sust, hbm, src = load_peaks()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
@@ -101,10 +103,11 @@ def main():
             extra = {k: int(v) for k, v in (kv.split("=") for kv in a.knobs.split(",") if kv)}
             grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=2, n_comm1=0, **extra))
             best = None
-            for nc0 in ([0] if par.world_size == 1 else [int(v) for v in a.nc0.split(",")]) * a.reps:
-                grp.set_knobs(LayerKnobs(n_comm0=nc0, n_comm1=0, **extra))
+            cands = [0] if par.world_size == 1 else ([None] if a.nc0 == "auto" else [int(v) for v in a.nc0.split(",")])
+            for nc0 in cands * a.reps:
+                grp.set_knobs(LayerKnobs.for_world(par.world_size, n_comm0=nc0, n_comm1=0, **extra))
                 r = grp.measure(iters=a.iters)
-                r["n_comm0"] = nc0
+                r["n_comm0"] = grp.layers[0].n_comm0(M) if nc0 is None else nc0
                 if best is None or r["latency_ms"] < best["latency_ms"]:
                     best = r
             rec = {"knobs": a.knobs, "shape": shape, "E": E, "topk": topk, "N": N, "K": K, "ep": ep, "tp": tp, "M": M, "std": std,
