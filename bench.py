@@ -478,7 +478,7 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "knobs": {"n_comm0": layer.split_choice(M)[0], "n_comm0_source": layer.split_choice(M)[1],
-                      "n_comm1": knobs.n_comm1, "group0": knobs.group0,
+                      "n_comm1": knobs.n_comm1, "group0": layer.group0(M),
                       "wave1": knobs.wave1},
         }
         if cpu is not None:

@@ -95,6 +95,10 @@ class SplitRecord:
     optimal_nc: int
     latency_ns: int
     curve: Tuple[Tuple[int, int], ...]
+    # B200 extension (absent from the reference schema, optional in the
+    # JSON): the layer0 pair-group size the curve was measured at, chosen
+    # jointly with n_c by the sweep (the curve is the one at this group)
+    group0: Optional[int] = None
 
     def __post_init__(self) -> None:
         if not self.curve:
@@ -104,14 +108,18 @@ class SplitRecord:
             raise ConfigurationError("stored optimum is not the argmin of the stored curve")
 
     def to_json_dict(self) -> dict:
-        return {"key": self.key.to_json_dict(), "optimal_nc": self.optimal_nc,
-                "latency_ns": self.latency_ns, "curve": [list(pt) for pt in self.curve]}
+        out = {"key": self.key.to_json_dict(), "optimal_nc": self.optimal_nc,
+               "latency_ns": self.latency_ns, "curve": [list(pt) for pt in self.curve]}
+        if self.group0 is not None:
+            out["group0"] = self.group0
+        return out
 
     @classmethod
     def from_json_dict(cls, data: dict) -> "SplitRecord":
         return cls(key=SplitKey.from_json_dict(data["key"]), optimal_nc=int(data["optimal_nc"]),
                    latency_ns=int(data["latency_ns"]),
-                   curve=tuple((int(a), int(b)) for a, b in data["curve"]))
+                   curve=tuple((int(a), int(b)) for a, b in data["curve"]),
+                   group0=int(data["group0"]) if data.get("group0") is not None else None)
 
 
 @dataclass
@@ -160,17 +168,18 @@ def candidate_ncs(blocks: int, stride: int = 2, max_nc: Optional[int] = None) ->
     return out
 
 
-def record_from_curve(key: SplitKey, points: Sequence[Tuple[int, int]]) -> SplitRecord:
+def record_from_curve(key: SplitKey, points: Sequence[Tuple[int, int]], group0: Optional[int] = None) -> SplitRecord:
     curve = tuple(sorted((int(a), int(b)) for a, b in points))
     nc, ns = min(curve, key=lambda pt: (pt[1], pt[0]))
-    return SplitRecord(key=key, optimal_nc=nc, latency_ns=ns, curve=curve)
+    return SplitRecord(key=key, optimal_nc=nc, latency_ns=ns, curve=curve, group0=group0)
 
 
 def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSpec,
                 cost=None, cost_name: str = "b200", blocks: Optional[int] = None,
                 stride: int = 2, rank: int = 0, max_nc: int = 16, repeats: int = 5,
-                measure: Optional[Callable[[int], float]] = None,
-                candidates: Optional[Sequence[int]] = None) -> SplitRecord:
+                measure: Optional[Callable[..., float]] = None,
+                candidates: Optional[Sequence[int]] = None,
+                groups: Optional[Sequence[int]] = None) -> SplitRecord:
     """Measure the fused layer at each candidate n_c and record the argmin.
 
     ``measure(n_c) -> seconds`` defaults to timing the layer on this GPU with
@@ -180,6 +189,9 @@ def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSp
     defaults of ``LayerKnobs.for_world``).  ``candidates`` overrides the
     even grid ``candidate_ncs(blocks, stride, max_nc)``.  ``cost`` is
     accepted for signature compatibility with the reference and ignored.
+    ``groups`` (B200 extension): layer0 pair-group sizes swept jointly with
+    n_c (``measure(n_c, group0)``); the record keeps the curve of the best
+    group and that group in ``group0``.
     """
     if blocks is None:
         from . import _lib
@@ -187,9 +199,13 @@ def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSp
     if measure is None:
         measure = _default_measure(model, parallel, workload, repeats)
     cands = list(candidates) if candidates is not None else candidate_ncs(blocks, stride, max_nc)
-    points = [(nc, int(round(measure(nc) * 1e9))) for nc in cands]
     key = SplitKey.for_config(model, parallel, workload.M, cost_name, blocks)
-    return record_from_curve(key, points)
+    if not groups:
+        points = [(nc, int(round(measure(nc) * 1e9))) for nc in cands]
+        return record_from_curve(key, points)
+    curves = {g: [(nc, int(round(measure(nc, g) * 1e9))) for nc in cands] for g in groups}
+    best = min(groups, key=lambda g: (min(ns for _, ns in curves[g]), g))
+    return record_from_curve(key, curves[best], group0=best)
 
 
 def _default_measure(model, parallel, workload, repeats):
@@ -201,8 +217,8 @@ def _default_measure(model, parallel, workload, repeats):
     grp = EmulatedGroup(model, parallel, routing, seed=workload.seed + 2)
     base = LayerKnobs.for_world(parallel.world_size)
 
-    def measure(nc):
-        grp.set_knobs(dataclasses.replace(base, n_comm0=nc))
+    def measure(nc, group0=None):
+        grp.set_knobs(dataclasses.replace(base, n_comm0=nc, group0=group0))
         return grp.measure(iters=repeats)["latency_ms"] * 1e-3
     return measure
 
@@ -210,6 +226,12 @@ def _default_measure(model, parallel, workload, repeats):
 def select_split(metadata: SplitMetadata, query: SplitKey) -> KernelSplit:
     """Exact key, else nearest log2 token bucket (ties -> smaller M), else
     ``UnprofiledConfigError`` (ref assigner.py:260-292)."""
+    chosen = select_record(metadata, query)
+    return split_for(chosen.key.blocks, chosen.optimal_nc)
+
+
+def select_record(metadata: SplitMetadata, query: SplitKey) -> SplitRecord:
+    """The record ``select_split`` picks (same lookup rules)."""
     if not metadata.records:
         raise UnprofiledConfigError("split metadata is empty")
     compatible = [r for r in metadata.records if r.key.compatible(query)]
@@ -224,7 +246,7 @@ def select_split(metadata: SplitMetadata, query: SplitKey) -> KernelSplit:
         if query.m < 1:
             raise UnprofiledConfigError(f"cannot bucket a token count of {query.m}; profile it explicitly")
         chosen = min(compatible, key=lambda r: (abs(math.log2(query.m) - math.log2(r.key.m)), r.key.m))
-    return split_for(chosen.key.blocks, chosen.optimal_nc)
+    return chosen
 
 
 # ---------------------------------------------------------------------------
@@ -253,10 +275,27 @@ def choose_split(model: ModelConfig, parallel: ParallelSpec, m_tokens: int, bloc
     assigner.py:260-292); for an unprofiled shape the fitted b200 cost model
     (costmodel.predict_split) instead of ``UnprofiledConfigError``.  Returns
     (split, "measured" | "model")."""
+    split, src, _ = choose_knobs(model, parallel, m_tokens, blocks, metadata)
+    return split, src
+
+
+def default_group0(world: int) -> int:
+    """Layer0 pair-group size without a measured record: 8
+    pairs at EP = 1 and EP >= 8, 4 at EP = 2/4."""
+    return 8 if world == 1 or world >= 8 else 4
+
+
+def choose_knobs(model: ModelConfig, parallel: ParallelSpec, m_tokens: int, blocks: int,
+                 metadata: Optional[SplitMetadata] = None) -> Tuple[KernelSplit, str, int]:
+    """``choose_split`` plus the layer0 pair-group size measured with it
+    (the record's ``group0``; ``default_group0`` when the record has none or
+    the cost model answered)."""
     meta = metadata if metadata is not None else default_metadata()
     try:
-        return select_split(meta, SplitKey.for_config(model, parallel, m_tokens, "b200", blocks)), "measured"
+        rec = select_record(meta, SplitKey.for_config(model, parallel, m_tokens, "b200", blocks))
+        g0 = rec.group0 if rec.group0 is not None else default_group0(parallel.world_size)
+        return split_for(rec.key.blocks, rec.optimal_nc), "measured", g0
     except UnprofiledConfigError:
         from .costmodel import predict_split
         rec = predict_split(model, parallel, WorkloadSpec(M=max(1, m_tokens), seed=0))
-        return split_for(blocks, min(rec.optimal_nc, blocks - 2)), "model"
+        return split_for(blocks, min(rec.optimal_nc, blocks - 2)), "model", default_group0(parallel.world_size)

@@ -155,7 +155,7 @@ class LayerKnobs:
 
     n_comm0: Optional[int] = None  # None: the adaptive chooser (assigner.choose_split) per token count
     n_comm1: int = 0
-    group0: int = 4
+    group0: Optional[int] = None  # None: measured with n_c by the chooser (assigner.choose_knobs)
     wave1: int = 4
     zc_n_comm: int = 16
     zc_group0: int = 16
@@ -184,10 +184,9 @@ class LayerKnobs:
 
     @classmethod
     def for_world(cls, world: int, **options) -> "LayerKnobs":
-        """Measured defaults: n_comm0 left to the adaptive
-        chooser (measured split metadata, else the fitted cost model);
-        8-pair layer0 groups at EP=1 and EP>=8, 4-pair groups at EP=2/4."""
-        options.setdefault("group0", 8 if world == 1 or world >= 8 else 4)
+        """Measured defaults: n_comm0 and group0 left to the
+        adaptive chooser (measured split metadata, else the fitted cost model
+        and 8-pair layer0 groups at EP=1 / EP>=8, 4-pair groups at EP=2/4)."""
         return cls(**options)
 
     def options(self) -> Dict[str, Optional[int]]:
@@ -242,14 +241,29 @@ class MoELayer:
             return 0, "world1"
         if self.knobs.n_comm0 is not None:
             return self.knobs.n_comm0, "knob"
+        return self._chosen(M)[:2]
+
+    def group0(self, M: int) -> int:
+        """Layer0 pair-group size: the knob when set, else the one measured
+        with the chosen n_c (``assigner.choose_knobs``)."""
+        if self.knobs.group0 is not None:
+            return self.knobs.group0
+        if self.parallel.world_size == 1:
+            from .assigner import default_group0
+            return default_group0(1)
+        return self._chosen(M)[2]
+
+    def _chosen(self, M: int):
         hit = self._nc_cache.get(M)
         if hit is None:
-            from .assigner import choose_split
+            from .assigner import choose_knobs
             blocks = self.knobs.grid or _lib.device_info(self.device)["sms"]
-            split, src = choose_split(self.model, self.parallel, M, blocks)
-            # the kernel needs an even count leaving >= one compute pair
-            nc = max(2, min(split.n_c, (blocks // 2) // 2 * 2) // 2 * 2)
-            hit = self._nc_cache[M] = (nc, src)
+            split, src, g0 = choose_knobs(self.model, self.parallel, M, blocks)
+            # the kernel needs an even count leaving >= one compute pair; a
+            # reduced grid (ranks sharing one GPU) keeps half of it computing
+            cap = blocks - 2 if self.knobs.grid is None else (blocks // 2) // 2 * 2
+            nc = max(2, min(split.n_c, cap) // 2 * 2)
+            hit = self._nc_cache[M] = (nc, src, g0)
         return hit
 
     @property
@@ -300,7 +314,7 @@ class MoELayer:
         self.ctx.forward(experts, M, self.weights.w0t, self.weights.w1t, combine_w, y_local,
                          activation=self.act, n_comm0=self.n_comm0(M),
                          n_comm1=self.n_comm1(),
-                         group0=k.group0, wave1=k.wave1, stream=stream)
+                         group0=self.group0(M), wave1=k.wave1, stream=stream)
 
     def forward(self, x_local, experts, combine_w=None, M: Optional[int] = None):
         torch = self.torch
@@ -388,7 +402,7 @@ class MoELayer:
             # the dispatch CTAs also reduce the combine (they do not join the
             # GEMMs here): a small count
             self.ctx.forward_host(xb, ex.contiguous(), cw, out, M, self.weights.w0t, self.weights.w1t,
-                                  self.act, n_comm0=k.stream_n_comm, group0=k.group0,
+                                  self.act, n_comm0=k.stream_n_comm, group0=self.group0(M),
                                   wave1=k.wave1, chunks=max(1, min(64, M // 1024)))
             self._note_host_reader()
             return out
@@ -618,11 +632,11 @@ def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
         for layer, y in zip(layers, outs):
             k = layer.knobs
             layer.ctx.layers(layer.weights.w0t, layer.weights.w1t, cw, y, layer.act,
-                             layer.n_comm0(M), k.group0, k.wave1, stream=stream)
+                             layer.n_comm0(M), layer.group0(M), k.wave1, stream=stream)
     else:
         for layer in layers:
             k = layer.knobs
-            layer.ctx.layer0(layer.weights.w0t, layer.act, layer.n_comm0(M), k.group0, stream=stream)
+            layer.ctx.layer0(layer.weights.w0t, layer.act, layer.n_comm0(M), layer.group0(M), stream=stream)
         for layer, y in zip(layers, outs):
             k = layer.knobs
             layer.ctx.layer1(layer.weights.w1t, cw, y, layer.n_comm1(), k.wave1,

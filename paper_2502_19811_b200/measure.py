@@ -161,12 +161,12 @@ class EmulatedGroup:
             for l, y in zip(self.layers, self.ys):
                 k = l.knobs
                 timed("layers", lambda l=l, y=y, k=k: l.ctx.layers(l.weights.w0t, l.weights.w1t, None, y, l.act,
-                                                                   l.n_comm0(self.M), k.group0, k.wave1))
+                                                                   l.n_comm0(self.M), l.group0(self.M), k.wave1))
         else:
             for l in self.layers:
                 k = l.knobs
                 timed("layer0", lambda l=l, k=k: l.ctx.layer0(l.weights.w0t, l.act, l.n_comm0(self.M),
-                                                              k.group0))
+                                                              l.group0(self.M)))
             for l, y in zip(self.layers, self.ys):
                 timed("layer1", lambda l=l, y=y: l.ctx.layer1(l.weights.w1t, None, y, l.n_comm1(), l.knobs.wave1))
         for l, y in zip(self.layers, self.ys):

@@ -84,3 +84,24 @@ def test_product_chooser_uses_measured_metadata_then_cost_model():
     split, src = choose_split(odd, ParallelSpec(1, 4), 4096, 148)
     assert src == "model"
     assert split.n_c == costmodel.predict_split(odd, ParallelSpec(1, 4), WorkloadSpec(M=4096, seed=0)).optimal_nc
+
+
+def test_joint_group_sweep_and_record_round_trip():
+    """B200 extension: sweep_split over (n_c, group0) keeps the best group's
+    curve and the group; the JSON keeps the reference schema plus an
+    optional "group0"; choose_knobs returns it (default group otherwise)."""
+    from paper_2502_19811_b200.assigner import choose_knobs, default_group0
+    lat = {(nc, g): 1000 - 10 * nc + (0 if g == 4 else 50) for nc in (2, 4, 6) for g in (2, 4, 8)}
+    rec = sweep_split(MX, ParallelSpec(1, 8), WorkloadSpec(M=8192), blocks=148, candidates=[2, 4, 6],
+                      groups=[2, 4, 8], measure=lambda nc, g: lat[(nc, g)] * 1e-9)
+    assert (rec.optimal_nc, rec.group0, rec.latency_ns) == (6, 4, 940)
+    assert rec.curve == ((2, 980), (4, 960), (6, 940))
+    meta = SplitMetadata(records=[rec])
+    back = SplitMetadata.from_json_str(meta.to_json_str())
+    assert back.records == [rec]
+    split, src, g0 = choose_knobs(MX, ParallelSpec(1, 8), 8192, 148, meta)
+    assert (split.n_c, src, g0) == (6, "measured", 4)
+    plain = record_from_curve(key(8192), [(2, 5), (4, 3)])
+    assert "group0" not in plain.to_json_dict()
+    split, src, g0 = choose_knobs(MX, ParallelSpec(1, 8), 8192, 148, SplitMetadata(records=[plain]))
+    assert (split.n_c, g0) == (4, default_group0(8))

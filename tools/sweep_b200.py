@@ -25,7 +25,8 @@ from paper_2502_19811_b200 import ModelConfig, ParallelSpec, WorkloadSpec  # noq
 from paper_2502_19811_b200.assigner import SplitMetadata, sweep_split  # noqa: E402
 
 SHAPES = {"MX": (8, 2, 4096, 14336), "PH": (16, 2, 4096, 6400), "QW": (64, 8, 3584, 2560)}
-CANDIDATES = [4, 8, 16, 24, 32, 48, 64, 80, 96]
+CANDIDATES = [8, 16, 24, 32, 48, 64, 80, 96]
+GROUPS = [2, 4, 8]  # layer0 pair-group sizes swept jointly with n_c (SplitRecord.group0)
 
 
 def configs(quick):
@@ -51,10 +52,11 @@ def main():
         model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
         t0 = time.time()
         rec = sweep_split(model, ParallelSpec(tp=tp, ep=ep), WorkloadSpec(M=M, seed=0, std=0.0),
-                          cost_name="b200", candidates=CANDIDATES, repeats=a.repeats)
+                          cost_name="b200", candidates=CANDIDATES, repeats=a.repeats, groups=GROUPS)
         meta.add(rec)
         torch.cuda.empty_cache()
         print(json.dumps({"shape": shape, "ep": ep, "tp": tp, "M": M, "optimal_nc": rec.optimal_nc,
+                          "group0": rec.group0,
                           "latency_ms": rec.latency_ns / 1e6, "curve_ms": {nc: ns / 1e6 for nc, ns in rec.curve},
                           "wall_s": round(time.time() - t0, 1)}), flush=True)
         meta.save(a.out)
