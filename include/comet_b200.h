@@ -106,8 +106,10 @@ int comet_index_build(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_
  * flags bit0 = reference outputs (tiles0/tiles1/chunks and the global
  * counts / transfer matrix), bit1 = combine token list (needed by comm-CTA
  * combine), bit2 = publish this rank's token-ready epoch to the peers, bit3 =
- * streamed-forward pair order.  comet_index_build = flags 3; comet_forward
- * builds only what its kernels consume (counts / transfer are then stale). */
+ * streamed-forward pair order, bit6 = the layer1 pair order comet_forward
+ * uses (fold-level order per the FOLD_ORDER option).  comet_index_build =
+ * flags 3; comet_forward builds only what its kernels consume (counts /
+ * transfer are then stale). */
 int comet_index_build_ex(comet_ctx* ctx, const int32_t* d_experts, int M, int tile_rows, int tile_cols,
                          int flags, void* stream);
 /* Sizes of the index arrays after a build (synchronises the stream). */
@@ -236,7 +238,9 @@ int comet_device_info(int device, int32_t out[4]);
  *                  -1 automatic (default: on when a token can have several
  *                  hosted rows on a rank), 0 off, 1 on
  *   PULL_LOCAL     world > 1: dispatch CTAs place the local rows too (1)
- *   FOLD_ORDER     world > 1: layer1 pairs in fold-level order (1)
+ *   FOLD_ORDER     world > 1: layer1 pairs in fold-level order (0: its
+ *                  level computation costs the index build 8-12 us and
+ *                  PH EP4xTP2 ran 0.300 vs 0.282 ms, QW EP8 0.381 vs 0.376)
  *   GROUP1         layer1 pair-group size, 0 = layer0's group (0)
  *   CHUNK_ROWS     dispatch item rows 1..32 (32)
  *   PDL            programmatic dependent launch bitmask: 1 local dispatch,

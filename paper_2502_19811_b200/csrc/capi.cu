@@ -71,7 +71,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // token chunks) read a previous chunk's index in dispatch_local -- kept off.
 constexpr int kOptDefaults[COMET_OPT_COUNT] = {
     /*FUSED*/ 1, /*KSPLIT_MAX*/ 8, /*SPLIT_TAIL0*/ 1, /*SPLIT1*/ -1, /*DEDUP*/ -1, /*PULL_LOCAL*/ 1,
-    /*FOLD_ORDER*/ 1, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 6, /*GRID*/ 0, /*FUSE1*/ 0,
+    /*FOLD_ORDER*/ 0, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 6, /*GRID*/ 0, /*FUSE1*/ 0,
     /*SPIN_TIMEOUT_MS*/ 600000, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
     /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0, /*STREAMK*/ 0};
 
@@ -579,9 +579,19 @@ int comet_index_build(comet_ctx* x, const int32_t* d_experts, int M, int tile_ro
   return comet_index_build_ex(x, d_experts, M, tile_rows, tile_cols, kIndexRefLists | kIndexCombineList, stream);
 }
 
+// Layer1 pair-order bit of comet_forward's index build: world > 1 with fold
+// chains (several hosted experts per token) orders the layer1 pairs by fold
+// level when COMET_OPT_FOLD_ORDER is set.
+static int forward_order_flags(const comet_ctx* x) {
+  const bool fold_order = x->cfg.world > 1 && x->E_r > 1 && x->E_r <= 64 && x->cfg.topk > 1 &&
+                          x->opt[COMET_OPT_FOLD_ORDER] != 0;
+  return fold_order ? kIndexFoldOrder : 0;
+}
+
 int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile_rows, int tile_cols, int flags,
                          void* stream) {
   const auto& c = x->cfg;
+  if (flags & kIndexForwardOrder) flags = (flags & ~kIndexForwardOrder) | forward_order_flags(x);
   if (M < 0 || M > c.m_cap) return fail(COMET_EINVAL, "M=%d outside [0, m_cap=%d]", M, c.m_cap);
   if (tile_rows < 1) return fail(COMET_EINVAL, "tile_rows must be >= 1, got %d", tile_rows);
   if (tile_cols < 1 || tile_cols > c.N) return fail(COMET_EINVAL, "tile_cols must be in [1, %d], got %d", c.N, tile_cols);
@@ -1023,12 +1033,8 @@ int comet_forward(comet_ctx* x, const int32_t* d_experts, int M, const void* w0t
                   int wave1, void* stream) {
   // hot path: no reference-format tile lists; combine list only for comm-CTA combine
   // (the combine list only feeds world-1 combine CTAs; world > 1 fuses the combine)
-  // world > 1 with fold chains (several hosted experts per token): order the
-  // layer1 pairs by fold level (COMET_FOLD_ORDER=0 keeps expert order)
-  const bool fold_order = x->cfg.world > 1 && x->E_r > 1 && x->E_r <= 64 && x->cfg.topk > 1 &&
-                          x->opt[COMET_OPT_FOLD_ORDER] != 0;
   const int flags = (x->cfg.world == 1 && n_comm1 > 0 ? kIndexCombineList : 0) |
-                    (x->cfg.world > 1 ? kIndexSignal : 0) | (fold_order ? kIndexFoldOrder : 0);
+                    (x->cfg.world > 1 ? kIndexSignal : 0) | forward_order_flags(x);
   if (int rc = comet_index_build_ex(x, d_experts, M, 128, x->cfg.N >= 512 ? 128 : std::max(1, x->cfg.N / 4), flags,
                                     stream))
     return rc;

@@ -33,6 +33,7 @@ constexpr int kIndexCombineList = 2;   // combine token list (comm-CTA combine)
 constexpr int kIndexSignal = 4;        // publish this rank's x_ready epoch to every peer
 constexpr int kIndexStream = 8;        // host-streamed forward: pairs in (row tile, expert) order
 constexpr int kIndexFoldOrder = 16;    // fused combine with fold chains: order pairs1 by fold level
+constexpr int kIndexForwardOrder = 64; // host flag: add comet_forward's fold-order bit (COMET_OPT_FOLD_ORDER)
                                        // (experts whose rows are only folded in come first) and,
                                        // per token, the fused-combine folder = its row claimed LAST
 constexpr int kIndexMaxChunks = 64;    // token chunks per hosted expert (host-checked)

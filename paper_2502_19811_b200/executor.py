@@ -614,8 +614,9 @@ def run_emulated(x, weights, routing: RoutingTable, parallel: ParallelSpec,
 
 def index_flags(world: int, n_comm1: int) -> int:
     """Index-build flags of the forward hot path (index.cuh): combine token
-    list only for world-1 combine CTAs; x_ready signal when world > 1."""
-    return (2 if world == 1 and n_comm1 > 0 else 0) | (4 if world > 1 else 0)
+    list only for world-1 combine CTAs; x_ready signal when world > 1; the
+    layer1 pair order comet_forward uses (kIndexForwardOrder)."""
+    return (2 if world == 1 and n_comm1 > 0 else 0) | (4 if world > 1 else 0) | 64
 
 
 def _phase_forward(layers, ex, M: int, outs, cw, stream=None) -> None:
