@@ -188,7 +188,8 @@ struct comet_ctx {
   float* cw_dev = nullptr;                 // uploaded combine weights
   __nv_bfloat16* y_stream = nullptr;       // [m_cap, N] output of the streamed forward
   float* part = nullptr;       // split-K partials: 2 layers x (pairs x 2 CTA tiles) x 128 x 512 fp32
-  uint32_t* split_cnt = nullptr;  // 2 layers x 512 slice counters (reset by each tile's finisher)
+  uint32_t* split_cnt = nullptr;  // 2 layers x 1024 slice counters: [tile] arrived / finished, [256 + tile]
+                                  // landed, [512 + 2 tile + half] finished chunks (reset by their last user)
   int n_h = 0;
   // layer-kernel launch timing (comet_kernel_timing_*): an event pair around
   // each moe_layer_kernel launch, on the launch stream, in a ring of slots
@@ -699,8 +700,8 @@ static int ensure_work(comet_ctx* x) {
   // layer needs at most (grid/2 pairs) x 2 CTA tiles of 128 x 512 fp32;
   // layer1 also holds the stream-K tail's partials: two per range, ranges <= pairs
   CK(cudaMalloc(&x->part, (size_t)3 * x->n_sm * kTileRows * kBlockN * sizeof(float)));
-  CK(cudaMalloc(&x->split_cnt, sizeof(uint32_t) * 2 * 512));
-  CK(cudaMemset(x->split_cnt, 0, sizeof(uint32_t) * 2 * 512));
+  CK(cudaMalloc(&x->split_cnt, sizeof(uint32_t) * 2 * 1024));
+  CK(cudaMemset(x->split_cnt, 0, sizeof(uint32_t) * 2 * 1024));
   int rc = make_map(&x->tm_xs, x->xs, c.m_cap, c.N, 1);
   if (!rc) rc = make_map(&x->tm_xg, x->xg, x->cap_rows_pad, c.N, 128);
   if (!rc) rc = make_map(&x->tm_H, x->H, x->cap_rows_pad, x->k_local, 128);
@@ -847,7 +848,7 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   LayerArgs a = base_args(x);
   a.layer = 1;
   a.part = x->part + (size_t)x->n_sm * kTileRows * kBlockN;
-  a.split_cnt = x->split_cnt + 512;
+  a.split_cnt = x->split_cnt + 1024;
   a.streamk = x->opt[COMET_OPT_STREAMK] != 0;
   a.n_blocks = x->nb1;
   a.k_blocks = x->kb1;

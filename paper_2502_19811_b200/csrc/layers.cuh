@@ -43,7 +43,7 @@ struct LayerArgs {
   int ksplit_max;         // split-K slices allowed when output tiles are fewer than pairs (0 = off)
   int streamk;            // layer1: stream-K tail (sched.cuh) instead of whole units in the last round
   float* part;            // split-K fp32 partials [tiles*NB][S][128][512] (<= pairs*2 CTA tiles)
-  uint32_t* split_cnt;    // [tiles*NB] slices landed (reset by the finisher)
+  uint32_t* split_cnt;    // [1024] split-K counters of this layer (capi.cu comet_ctx::split_cnt)
   uint32_t epoch;
   int debug;              // timing-experiment bits, compiled in only with -DCOMET_TIMING_EXPERIMENTS
                           // (COMET_DBG; wrong results unless noted): 1: comm CTAs idle; 4: spin

@@ -111,6 +111,10 @@ __device__ __forceinline__ void fold_regs(uint32_t (&acc)[32], const uint4* r, f
   }
 }
 constexpr int kMaxFold = 7;  // earlier hosted rows of a token (top-k <= 8)
+#ifndef COMET_HELP_POLL_NS
+#define COMET_HELP_POLL_NS 3000
+#endif
+constexpr uint64_t kHelpPollNs = COMET_HELP_POLL_NS;  // split-K: how long an earlier slice polls for the last one
 
 constexpr int kSchedSlots = 2;
 constexpr int kLifeTask = (1 << 20) - 2;  // timeline task id of a CTA's lifetime record
@@ -478,7 +482,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // contiguous destination rows (H, or yrows without the fused combine):
       // TMA tensor stores; fused-combine units write scattered token rows
       const bool tma_out = (w.layer == 0 || !p.fuse_combine) && !COMET_DBG(p.debug, 16384);
-      auto process = [&](int s, uint32_t (&v0)[32], uint32_t (&v1)[32]) {
+      auto process = [&](int s, int seq, uint32_t (&v0)[32], uint32_t (&v1)[32]) {
         if (w.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -521,10 +525,12 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // row's 128 B (XOR-swizzled 16 B granules, conflict-free), then each
         // store instruction writes 4 whole 128 B lines (8 lanes per row).
         // Only this warp touches its staging rows: __syncwarp suffices.
-        uint8_t* stg = epi_smem + ((s & 1) * 4 + ew) * kSmemEpiWarp;
-        // TMA store: the staging rows (SW128 layout) of chunk s-2 must be
+        // (seq: this epilogue's count of processed chunks -- the staging
+        // buffer alternates per processed chunk, not per column chunk)
+        uint8_t* stg = epi_smem + ((seq & 1) * 4 + ew) * kSmemEpiWarp;
+        // TMA store: the staging rows (SW128 layout) of chunk seq-2 must be
         // read out before they are overwritten
-        if (tma_out && s >= 2) {
+        if (tma_out && seq >= 2) {
           if (lane == 0) ptx::bulk_wait_read<1>();
           __syncwarp();
         }
@@ -565,9 +571,6 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // split-K: this slice's fp32 partial of the CTA's 128 x 512 tile, stored
       // column-quad major ([c/4][row][4]) so a warp's 32 rows of one quad are
       // 512 contiguous bytes (coalesced stores and reloads)
-      // split-K: this slice's fp32 partial of the CTA's 128 x 512 tile, stored
-      // column-quad major ([c/4][row][4]) so a warp's 32 rows of one quad are
-      // 512 contiguous bytes (coalesced stores and reloads)
       const int S = w.np;
       const long long split_tile = static_cast<long long>(row0 >> 7) * NB + w.nb;
       float4* part_row = S > 1 ? reinterpret_cast<float4*>(p.part + (split_tile * S + w.ks) * kTileRows * kBlockN) +
@@ -581,10 +584,16 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // + slice 1: IEEE addition commutes, so the value is the same whichever
       // slice finishes -- bitwise deterministic), so its own partial is never
       // written and re-read.  More slices (small-M split-K): every slice
-      // stores its partial; the last to land sums all S in slice order after
-      // its accumulator is released.
+      // stores its partial; the tile's 64-column chunks -- each the sum of
+      // all S partials in slice order (deterministic) -- are finished by the
+      // last slice to arrive and by earlier slices that see it arrive (see
+      // below), so the reduction is spread over the slices (one CTA summing
+      // all S x 8 chunks was ~40 us of dependent loads at the end of small-M
+      // forwards); a half's completion is counted per chunk and published by
+      // the CTA that completes it.
       const bool early = S == 2;
       bool finisher = S == 1;  // this CTA produces the tile's output (always, without split-K)
+      uint32_t split_done = 0u;  // S > 2: the 256-column halves whose last chunk this slice finished
       uint32_t* landed = p.split_cnt + 256 + split_tile;
       const float4* rows0 =
           S > 1 ? reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + ew * 32 + lane : nullptr;
@@ -666,7 +675,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
             }
           }
         }
-        process(s, v0, v1);
+        process(s, s, v0, v1);
       }
       if (tma_out) {  // this warp's tensor stores complete before the unit is counted
         if (lane == 0) ptx::bulk_wait<0>();
@@ -682,16 +691,40 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           *landed = 0u;
         }
       } else if (S > 1) {
+        // Partial stored -> arrive (acq_rel: the arrival count implies every
+        // earlier arriver's partial is visible).  The last arriver finishes
+        // the tile's chunks; an earlier arriver polls for the last arrival
+        // for a few us and, if it sees it, helps: chunks are claimed one at a
+        // time from a per-tile counter.  Nobody waits on a slice that has
+        // not arrived beyond that bounded poll, so two slices of one tile
+        // queued on one pair (consecutive claims of short slices) cannot
+        // deadlock.  Every counter is reset by the launch's last CTA out.
         __threadfence();
         ptx::named_bar_sync(1, 128);
-        if (threadIdx.x == kEpiThread0) *sflag = atomicAdd(p.split_cnt + split_tile, 1u) == static_cast<uint32_t>(S - 1);
+        if (threadIdx.x == kEpiThread0) {
+          uint32_t* arrive = p.split_cnt + split_tile;
+          bool help = ptx::atom_acq_rel_gpu_add(arrive, 1u) == static_cast<uint32_t>(S - 1);
+          if (!help) {
+            const uint64_t t0 = ptx::globaltimer();
+            while (!(help = ptx::ld_acquire_gpu(arrive) >= static_cast<uint32_t>(S)) &&
+                   ptx::globaltimer() - t0 < kHelpPollNs) {
+            }
+          }
+          *sflag = help;
+        }
         ptx::named_bar_sync(1, 128);
-        finisher = *reinterpret_cast<volatile int*>(sflag) != 0;
-        if (finisher) {
+        const bool help = *reinterpret_cast<volatile int*>(sflag) != 0;
+        int mine[2] = {0, 0};  // chunks this CTA finished per 256-column half
+        if (help) {
           __threadfence();
           fold_wait();
-#pragma unroll 1
-          for (int s = 0; s < n_chunks; ++s) {
+          uint32_t* next = p.split_cnt + 256 + split_tile;
+          for (int seq = 0;; ++seq) {
+            ptx::named_bar_sync(1, 128);  // the previous claim was read by every thread
+            if (threadIdx.x == kEpiThread0) *sflag = static_cast<int>(atomicAdd(next, 1u));
+            ptx::named_bar_sync(1, 128);
+            const int s = *reinterpret_cast<volatile int*>(sflag);
+            if (s >= n_chunks) break;
             if (s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;
             uint32_t v0[32], v1[32];
             float acc[64];
@@ -710,18 +743,40 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
               v0[i] = __float_as_uint(acc[i]);
               v1[i] = __float_as_uint(acc[32 + i]);
             }
-            process(s, v0, v1);
+            process(s, seq, v0, v1);
+            ++mine[w.half >= 0 ? w.half : (s * 64 >= static_cast<int>(kHalfN) ? 1 : 0)];
           }
           if (tma_out) {
             if (lane == 0) ptx::bulk_wait<0>();
             __syncwarp();
           }
-          if (threadIdx.x == kEpiThread0) p.split_cnt[split_tile] = 0u;  // ready for the next launch
         }
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (threadIdx.x == kEpiThread0) {
+          // a half is complete when all of its real chunks are (any CTA)
+          uint32_t done = 0u;
+          uint32_t* hc = p.split_cnt + 512 + 2 * split_tile;
+          for (int h = 0; h < 2; ++h) {
+            if (!mine[h]) continue;
+            int real = 0;
+            for (int c = 0; c < n_chunks; ++c)
+              real += c * 64 < cols_left && (w.half >= 0 ? w.half : (c * 64 >= static_cast<int>(kHalfN) ? 1 : 0)) == h;
+            if (atomicAdd(hc + h, static_cast<uint32_t>(mine[h])) + mine[h] == static_cast<uint32_t>(real)) done |= 1u << h;
+          }
+          *sflag = static_cast<int>(done);
+        }
+        ptx::named_bar_sync(1, 128);
+        split_done = static_cast<uint32_t>(*reinterpret_cast<volatile int*>(sflag));
       }
       // completion counted in real 256-column halves (half 1 of a narrow last
-      // block -- a split-tail half -- covers none); split-K: by the finisher
-      const uint32_t amount = !finisher ? 0u : w.half < 0 ? 2u : ((w.half == 1 && narrow_block(p, w.nb)) ? 0u : 1u);
+      // block -- a split-tail half -- covers none); split-K: by the finisher,
+      // or (S > 2) per half by the slice that completed it
+      const uint32_t done_mask = S > 2 ? split_done
+                                 : !finisher ? 0u
+                                 : w.half < 0 ? 3u
+                                 : ((w.half == 1 && narrow_block(p, w.nb)) ? 0u : (1u << w.half));
+      const uint32_t amount = __popc(done_mask);
       if (w.layer == 0 && f.mode == 2) {
         // this CTA's 128 H rows of the unit's columns are in memory -> count
         // them for the layer1 units that read the tile as their A operand
@@ -761,8 +816,9 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           __threadfence();
           ptx::red_release_gpu_add(p.nb_done + w.nb, amount);
           if (p.fuse_combine || p.publish_tiles)
-            for (int h = h_lo; h <= h_hi; ++h)
-              ptx::st_release_gpu(p.tile_done + (static_cast<long long>(row0 >> 7) * NB + w.nb) * 2 + h, p.epoch);
+            for (int h = 0; h < 2; ++h)
+              if ((done_mask >> h) & 1u)
+                ptx::st_release_gpu(p.tile_done + (static_cast<long long>(row0 >> 7) * NB + w.nb) * 2 + h, p.epoch);
           if (p.world > 1)
             comm::nb_contributed(p, w.nb, amount,
                                  (narrow_block(p, w.nb) ? 2u : 4u) * static_cast<uint32_t>(P) +
@@ -833,6 +889,9 @@ moe_layer_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constan
   __syncthreads();
   if (s_last) {
     for (int i = threadIdx.x; i < f.n_h; i += blockDim.x) f.h_cnt[i] = 0u;
+    for (int l = 0; l < 2; ++l)  // split-K counters (arrivals, chunk claims, finished chunks)
+      if (f.l[l].split_cnt)
+        for (int i = threadIdx.x; i < 1024; i += blockDim.x) f.l[l].split_cnt[i] = 0u;
     if (threadIdx.x == 0) {
       f.sched[0] = 0u;
       f.sched[1] = 0u;

@@ -293,6 +293,26 @@ def test_split_k_small_m(tp, ep, M):
     assert_close(ys[2], ref, what=f"unsplit tp={tp} ep={ep} M={M}")
 
 
+@pytest.mark.parametrize("ks", [3, 5, 6])
+def test_split_k_slice_counts(ks):
+    """S > 2 slices finish the tile's 64-column chunks round robin (chunk c
+    by slice c mod S, sum of all S partials in slice order): every slice
+    count, including ones that do not divide the 8 chunks, matches the
+    oracle, is run-to-run bitwise deterministic, and equals the S = 8 result
+    up to the fp32 partial-sum order (tolerance)."""
+    model = ModelConfig(L=1, E=8, topk=2, N=512, K=2048)
+    par = ParallelSpec(1, 8)
+    routing = build_routing(model, par, WorkloadSpec(M=300, seed=61, std=0.0))
+    w = random_weights(model, seed=62)
+    x = np.random.default_rng(63).standard_normal((300, 512))
+    cw = np.random.default_rng(64).random((300, 2))
+    ys = [run_emulated(x, w, routing, par, combine_weights=cw,
+                       knobs=LayerKnobs(n_comm0=8, n_comm1=0, ksplit_max=ks)).cpu().numpy() for _ in range(2)]
+    np.testing.assert_array_equal(ys[0], ys[1])
+    ref = oracle_bf16_inputs(x, w.w0, w.w1, routing.as_array(), None, cw)
+    assert_close(ys[0], ref, what=f"split-K S<={ks}")
+
+
 @pytest.mark.parametrize("E,topk,M,N,K", [(8, 2, 5000, 512, 1024), (8, 3, 3000, 512, 2048), (16, 4, 700, 256, 512),
                                           (8, 2, 100, 512, 2048)])
 def test_streamed_host_forward(E, topk, M, N, K):
