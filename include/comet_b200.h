@@ -244,7 +244,7 @@ int comet_device_info(int device, int32_t out[4]);
  *   GROUP1         layer1 pair-group size, 0 = layer0's group (0)
  *   CHUNK_ROWS     dispatch item rows 1..32 (32)
  *   PDL            programmatic dependent launch bitmask: 1 local dispatch,
- *                  2 layer kernel, 4 combine kernels (6)
+ *                  2 layer kernel, 4 combine kernels, 8 index build (14)
  *   GRID           cap on the persistent grid in CTAs, 0 = every SM (0)
  *   FUSE1          world 1: fused epilogue combine instead of the combine
  *                  kernel (0)

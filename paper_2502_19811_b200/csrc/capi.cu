@@ -67,18 +67,18 @@ constexpr size_t kIndexSmem = 8192 * sizeof(long long);
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Option defaults (comet_b200.h COMET_OPT_*), all measured (DESIGN.md §4/§6).
-// PDL default 6: with bit 1 the host-pipeline test (forward_host, uneven
+// PDL default 14: with bit 1 the host-pipeline test (forward_host, uneven
 // token chunks) read a previous chunk's index in dispatch_local -- kept off.
 constexpr int kOptDefaults[COMET_OPT_COUNT] = {
     /*FUSED*/ 1, /*KSPLIT_MAX*/ 8, /*SPLIT_TAIL0*/ 1, /*SPLIT1*/ -1, /*DEDUP*/ -1, /*PULL_LOCAL*/ 1,
-    /*FOLD_ORDER*/ 0, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 6, /*GRID*/ 0, /*FUSE1*/ 0,
+    /*FOLD_ORDER*/ 0, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 14, /*GRID*/ 0, /*FUSE1*/ 0,
     /*SPIN_TIMEOUT_MS*/ 600000, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
     /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0, /*STREAMK*/ 0};
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous one drains; it calls griddepcontrol.wait before touching
 // the previous kernel's results.  `pdl` is the context's PDL bitmask
-// (COMET_OPT_PDL): 1 dispatch_local, 2 layer kernel, 4 combine kernels.
+// (COMET_OPT_PDL): 1 dispatch_local, 2 layer kernel, 4 combine kernels, 8 index build.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(int pdl, int bit, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -373,6 +373,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       {&ix.meta, (size_t)kMetaSlots},
       {&ix.chunk_cnt, (size_t)x->E_r * kIndexMaxChunks},
       {&ix.chunk_loc, (size_t)x->E_r * kIndexMaxChunks},
+      {reinterpret_cast<int32_t**>(&ix.chunk_flag), (size_t)x->E_r * kIndexMaxChunks},
       {&ix.pair_key, (size_t)x->cap_pairs},
       {reinterpret_cast<int32_t**>(&ix.fold_part), (size_t)2 * 160 * std::min(x->E_r, 64)},
   };
@@ -389,7 +390,6 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       b += align_up(p.n * 4, 256);
     }
     ix.done = reinterpret_cast<uint32_t*>(b);
-    ix.gbar = ix.done + 1;
   }
   ix.cap_rows = x->cap_rows;
   ix.cap_rows_pad = x->cap_rows_pad;
@@ -625,7 +625,8 @@ int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile
   // global histogram + transfer matrix accumulate by atomics: zero both (adjacent)
   const size_t zbytes = reinterpret_cast<char*>(x->ix.transfer + c.world * c.world) - reinterpret_cast<char*>(x->ix.counts);
   if (flags & kIndexRefLists) CK(cudaMemsetAsync(x->ix.counts, 0, zbytes, static_cast<cudaStream_t>(stream)));
-  index_build_kernel<<<grid, kIndexThreads, kIndexSmem, static_cast<cudaStream_t>(stream)>>>(ix);
+  CK(launch_pdl(x->opt[COMET_OPT_PDL], 8, index_build_kernel, dim3(grid), dim3(kIndexThreads), kIndexSmem,
+                static_cast<cudaStream_t>(stream), ix));
   CK(cudaGetLastError());
   x->ix.experts = d_experts;  // the layer1 finish kernel reads the global routing
   return COMET_OK;

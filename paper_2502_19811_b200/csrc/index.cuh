@@ -76,9 +76,9 @@ struct IndexDev {
   // scratch
   int32_t* pair_key;    // [P_cap]
   uint32_t* done;       // [1] CTA completion counter (self-resetting)
-  uint32_t* gbar;       // [2] grid barrier: arrival count (self-resetting), generation
   int32_t* chunk_cnt;   // [E_r * kIndexMaxChunks] hits per (hosted expert, token chunk)
   int32_t* chunk_loc;   // [E_r * kIndexMaxChunks] local-token hits per (hosted expert, chunk)
+  uint32_t* chunk_flag; // [E_r * kIndexMaxChunks] build epoch when the item's counts landed (look-back)
   unsigned long long* fold_part;  // [grid * E_r] per-CTA fold-predecessor masks (kIndexFoldOrder)
   uint32_t* zero_words; // layer1 per-n-block counters, zeroed every build
   int n_zero_words;

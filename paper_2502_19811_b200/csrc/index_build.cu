@@ -10,13 +10,15 @@
 // contiguous, rank-monotone blocks (routing.py:86-104), so ordering an
 // expert's rows by ((src - rank) mod W, token) is exactly the token order
 // rotated to start at this rank's first token.  Each expert's block is then a
-// stable stream compaction of the rotated token sequence -- one CTA per hosted
-// expert, block-wide ballot scans, no sort.
+// stable stream compaction of the rotated token sequence -- work items of
+// (hosted expert, token chunk), block-wide ballot scans, no sort.
 //
-// One launch: CTAs [0, E_r) build the per-expert layouts; CTA E_r writes the
-// global counts, the transfer matrix and the non-hosted slots; the last CTA
-// to finish (grid-wide completion counter) builds the tile lists, the 2-CTA
-// pair tables, the deduplicated NVLink pull list and the combine token list.
+// One launch: every CTA writes its token slice's non-hosted slots (and the
+// reference counts / transfer matrix when asked); each item counts its hits,
+// publishes them and looks back at the earlier items (decoupled look-back:
+// the rows before it, no grid barrier), then writes its rows; the last CTA to
+// finish (grid-wide completion counter) builds the tile lists, the 2-CTA
+// pair tables and the combine token list.
 #include <climits>
 #include <cstdint>
 
@@ -105,25 +107,6 @@ __device__ __forceinline__ uint64_t chunk_hits(const IndexDev& ix, int c, int T,
   return hit;
 }
 
-// Grid-wide barrier for the (co-resident, <= one CTA per SM) index grid:
-// generation counter, self-resetting arrival count.
-__device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t g = *reinterpret_cast<volatile uint32_t*>(gen);
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *reinterpret_cast<volatile uint32_t*>(count) = 0u;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      { ptx::Spin sp; while (*reinterpret_cast<volatile uint32_t*>(gen) == g) sp.pause(32, 13); }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
@@ -135,6 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   __shared__ int s_misc[8];
 
   ptx::pdl_launch_dependents();  // the dispatch / layer kernels may launch; they wait for this grid
+  // launched with programmatic serialization (COMET_OPT_PDL bit 8): only the
+  // launch overlapped the previous kernel (e.g. the last forward's combine),
+  // which may still read this rank's index -- wait for it before any write
+  ptx::pdl_wait();
   const int tid = threadIdx.x;
   unsigned long long tt0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));
@@ -159,21 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   if (blockIdx.x == 0)
     for (int i = tid; i < ix.n_zero_words; i += kThreads) ix.zero_words[i] = 0u;
 
-  // -------- phase 1a: per-(expert, chunk) hit counts --------
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
-    const int j = it / C, c = it - (it / C) * C;
-    int loc;
-    const uint64_t hit = chunk_hits(ix, c, T, TPT, ix.e_lo + j, start, n_own, &loc);
-    int tot, tot_loc;
-    block_scan(__popcll(hit), s_ws, &tot);
-    block_scan(loc, s_ws, &tot_loc);
-    if (tid == 0) {
-      ix.chunk_cnt[it] = tot;
-      ix.chunk_loc[it] = tot_loc;
-    }
-  }
   probe(0);
-  // -------- phase 1b: bookkeeping over natural token slices: global
+  // -------- phase 1 (independent of the row layout): bookkeeping over natural token slices: global
   // histogram (routing.py:78-84), transfer matrix (routing.py:106-117) and
   // the non-hosted tok_pos slots.  The hot path (no reference lists) needs
   // only the tok_pos slots --------
@@ -239,46 +213,46 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   }
 
   probe(1);
-  grid_barrier(ix.gbar, ix.gbar + 1);
-  probe(2);
 
-  // -------- phase 2: hosted offsets (every CTA), then stable compaction --------
-  for (int j = tid; j < Er; j += kThreads) {
-    int t = 0;
-    for (int c = 0; c < C; ++c) t += __ldcg(ix.chunk_cnt + j * C + c);
-    s_cnt[j] = t;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int o = 0, pd = 0;
-    for (int j = 0; j < Er; ++j) {
-      s_off[j] = o;
-      s_pad[j] = pd;
-      o += s_cnt[j];
-      pd += (s_cnt[j] + kPairRows - 1) / kPairRows * kPairRows;
-    }
-    s_off[Er] = o;
-    s_pad[Er] = pd;
-  }
-  __syncthreads();
+  // -------- rows: one pass per (hosted expert, token chunk) item.  Count the
+  // item's hits, publish the counts (epoch flag), look back at every earlier
+  // item (experts before j: their padded totals; chunks before c: the rows
+  // before this chunk -- a decoupled look-back, no grid barrier: every item
+  // waits only on lower items, so the lowest unfinished one never waits),
+  // then write the rows: a stable compaction of the rotated token order --------
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int j = it / C, c = it - (it / C) * C, e = ix.e_lo + j;
-    if (tid == 0) {
-      int before = 0;
-      for (int c2 = 0; c2 < c; ++c2) before += __ldcg(ix.chunk_cnt + j * C + c2);
-      s_misc[0] = before;
-      if (c == 0) {
-        int nl = 0;
-        for (int c2 = 0; c2 < C; ++c2) nl += __ldcg(ix.chunk_loc + j * C + c2);
-        ix.n_local[j] = nl;
-      }
-    }
     int loc;
     uint64_t hit = chunk_hits(ix, c, T, TPT, e, start, n_own, &loc);
-    int tot;
-    const int mine = block_scan(__popcll(hit), s_ws, &tot);  // (syncs: s_misc visible)
-    const int base_row = s_off[j], base_pad = s_pad[j];
-    int pos = s_misc[0] + mine;
+    int tot, tot_loc;
+    const int mine = block_scan(__popcll(hit), s_ws, &tot);
+    block_scan(loc, s_ws, &tot_loc);
+    if (tid == 0) {
+      ix.chunk_cnt[it] = tot;
+      ix.chunk_loc[it] = tot_loc;
+      ptx::st_release_gpu(ix.chunk_flag + it, ix.epoch);
+    }
+    for (int q = tid; q <= j; q += kThreads) s_cnt[q] = 0;
+    __syncthreads();
+    for (int q = tid; q < it; q += kThreads) {
+      { ptx::Spin sp; while (ptx::ld_acquire_gpu(ix.chunk_flag + q) != ix.epoch) sp.pause(32, 13); }
+      const int n = __ldcg(ix.chunk_cnt + q);
+      if (n) atomicAdd(s_cnt + q / C, n);  // experts < j: totals; expert j: rows before chunk c
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int o = 0, pd = 0;
+      for (int q = 0; q < j; ++q) {
+        o += s_cnt[q];
+        pd += (s_cnt[q] + kPairRows - 1) / kPairRows * kPairRows;
+      }
+      s_misc[0] = o;
+      s_misc[2] = pd;
+    }
+    __syncthreads();
+    const int before = s_cnt[j];
+    const int base_row = s_misc[0], base_pad = s_misc[2];
+    int pos = before + mine;
     while (hit) {
       const int q = __ffsll(hit) - 1;
       hit &= hit - 1;
@@ -305,14 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
       ix.tok_pos[static_cast<long long>(t) * K + sl] = base_pad + pos;
       ++pos;
     }
-    if (c == C - 1)  // padding rows of expert j's 256-aligned block
-      for (int r = base_pad + s_cnt[j] + tid; r < s_pad[j + 1]; r += kThreads)
+    if (c == C - 1) {  // padding rows of expert j's 256-aligned block
+      const int cnt = before + tot;
+      const int end = base_pad + (cnt + kPairRows - 1) / kPairRows * kPairRows;
+      for (int r = base_pad + cnt + tid; r < end; r += kThreads)
         if (r < ix.cap_rows_pad) {
           ix.gather_row[r] = -1;
           ix.row_dst[r] = -1;
           ix.row_widx[r] = 0;
         }
-    __syncthreads();  // s_misc reuse
+    }
+    __syncthreads();  // s_cnt / s_misc reuse
   }
 
   probe(3);
@@ -327,6 +304,31 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   if (!s_misc[1]) return;
   __threadfence();
   probe(4);
+  // every item landed: expert totals, row / padded offsets, local prefixes
+  __shared__ int s_nloc[kMaxExperts];
+  for (int j = tid; j < Er; j += kThreads) {
+    int t = 0, nl = 0;
+    for (int c = 0; c < C; ++c) {
+      t += __ldcg(ix.chunk_cnt + j * C + c);
+      nl += __ldcg(ix.chunk_loc + j * C + c);
+    }
+    s_cnt[j] = t;
+    s_nloc[j] = nl;
+    ix.n_local[j] = nl;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0, pd = 0;
+    for (int j = 0; j < Er; ++j) {
+      s_off[j] = o;
+      s_pad[j] = pd;
+      o += s_cnt[j];
+      pd += (s_cnt[j] + kPairRows - 1) / kPairRows * kPairRows;
+    }
+    s_off[Er] = o;
+    s_pad[Er] = pd;
+  }
+  __syncthreads();
   for (int j = tid; j <= Er; j += kThreads) {
     ix.row_off[j] = s_off[j];
     ix.pad_off[j] = s_pad[j];
@@ -336,9 +338,6 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   // tiles per expert (reference tile_rows) and pairs per expert (256 rows)
   __shared__ int s_t0[kMaxExperts + 1];
   __shared__ int s_p0[kMaxExperts + 1];
-  __shared__ int s_nloc[kMaxExperts];
-  for (int j = tid; j < Er; j += kThreads) s_nloc[j] = __ldcg(ix.n_local + j);
-  __syncthreads();
   if (tid == 0) {
     int t = 0, p = 0;
     for (int j = 0; j < Er; ++j) {
