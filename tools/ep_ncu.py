@@ -1,5 +1,10 @@
-"""One emulated EP forward for ncu: 2 warm forwards, then the profiled one
-(capture rank 0's layer kernel with -k regex:moe_layer -s <2*W> -c 1)."""
+"""One emulated EP forward for ncu, product knobs (LayerKnobs.for_world:
+chooser n_c and pair group): 3 warm forwards, then the profiled one (capture
+rank 0's layer kernel with -k regex:moe_layer -s <3*ranks> -c 1).
+
+    python tools/ep_ncu.py [--shape MX] [--ep 8] [--tp 1] [--M 8192]
+"""
+import argparse
 import os
 import sys
 
@@ -9,12 +14,19 @@ import torch  # noqa: E402
 from paper_2502_19811_b200 import LayerKnobs, ModelConfig, ParallelSpec, WorkloadSpec, build_routing  # noqa: E402
 from paper_2502_19811_b200.measure import EmulatedGroup  # noqa: E402
 
-ep = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-model = ModelConfig(L=1, E=8, topk=2, N=4096, K=14336)
-par = ParallelSpec(1, ep)
-routing = build_routing(model, par, WorkloadSpec(M=8192, seed=0))
-grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=64, group0=4))
-for _ in range(3):
+SHAPES = {"MX": (8, 2, 4096, 14336), "PH": (16, 2, 4096, 6400), "QW": (64, 8, 3584, 2560)}
+ap = argparse.ArgumentParser()
+ap.add_argument("--shape", default="MX")
+ap.add_argument("--ep", type=int, default=8)
+ap.add_argument("--tp", type=int, default=1)
+ap.add_argument("--M", type=int, default=8192)
+a = ap.parse_args()
+E, topk, N, K = SHAPES[a.shape]
+model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
+par = ParallelSpec(a.tp, a.ep)
+routing = build_routing(model, par, WorkloadSpec(M=a.M, seed=0))
+grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs.for_world(par.world_size))
+for _ in range(4):
     grp._forward_timed(False)
 torch.cuda.synchronize()
-print("done")
+print("done", a.shape, a.ep, a.tp, "n_c", grp.layers[0].n_comm0(a.M), "group0", grp.layers[0].group0(a.M))
