@@ -58,7 +58,7 @@ int fail(int code, const char* fmt, ...) {
                                        __FILE__, __LINE__);                                   \
   } while (0)
 
-constexpr int kLayerThreads = 256;
+constexpr int kLayerThreads = 384;  // moe_layers.cu kThreads: 4 control + 8 epilogue warps
 constexpr int kMaxStreamChunks = 64;  // token chunks of the host-streamed forward
 constexpr size_t kLayerSmem = kLayerStages * 49152 + 32768 + 1024 + 1024;
 constexpr int kIndexThreads = 1024;
@@ -69,10 +69,13 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // Option defaults (comet_b200.h COMET_OPT_*), all measured (DESIGN.md §4/§6).
 // PDL default 14: with bit 1 the host-pipeline test (forward_host, uneven
 // token chunks) read a previous chunk's index in dispatch_local -- kept off.
+#ifndef COMET_DEFAULT_SPIN_MS
+#define COMET_DEFAULT_SPIN_MS 600000  // developer builds may shorten it (-DCOMET_DEFAULT_SPIN_MS=10000)
+#endif
 constexpr int kOptDefaults[COMET_OPT_COUNT] = {
     /*FUSED*/ 1, /*KSPLIT_MAX*/ 8, /*SPLIT_TAIL0*/ 1, /*SPLIT1*/ -1, /*DEDUP*/ -1, /*PULL_LOCAL*/ 1,
     /*FOLD_ORDER*/ 0, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 32, /*PDL*/ 14, /*GRID*/ 0, /*FUSE1*/ 0,
-    /*SPIN_TIMEOUT_MS*/ 600000, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
+    /*SPIN_TIMEOUT_MS*/ COMET_DEFAULT_SPIN_MS, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
     /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0, /*STREAMK*/ 0};
 
 // Launch with programmatic stream serialization (PDL): the kernel may start

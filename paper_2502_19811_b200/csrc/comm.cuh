@@ -15,7 +15,7 @@ namespace comet {
 namespace comm {
 
 constexpr int kMaxSlots = 224;
-constexpr int kReducers = 7;               // combine: warps 1..7
+constexpr int kReducers = 7;               // combine: warps 1..7 (higher warps idle)
 constexpr int kBatch = 16;                 // jobs described per loader pass
 constexpr uint32_t kRingBytes = 192 * 1024;
 #ifndef COMET_FREE_LAG
@@ -519,6 +519,7 @@ __device__ void combine_reduce(const LayerArgs& p, uint8_t* smem) {
     return;
   }
   // ---- reducers: warp w takes jobs k with k % kReducers == w - 1 ----
+  if (warp > kReducers) return;  // the layer kernel has more warps than reducers
   const int me = warp - 1;
   int k = 0;
   for (int nb = 0; nb < NB; ++nb) {
@@ -635,6 +636,7 @@ __device__ void stream_combine(const LayerArgs& p, uint8_t* smem) {
     }
     return;
   }
+  if (warp > kReducers) return;  // the layer kernel has more warps than reducers
   const int me = warp - 1;
   int k = 0;
   for (int c = 0; c < n_ch; ++c) {

@@ -41,7 +41,22 @@ namespace {
 // 128 A + 256 B rows for 128x512 MACs: 48 B/cycle at full rate instead of 64
 // for a 256x256 pair tile (the L2->SM traffic and the power that costs set the
 // sustained clock under the 1 kW cap).
-constexpr int kThreads = 256;
+// 12 warps: warp 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 unit
+// scheduler (warpgroup 0, shrunk to kRegsCtl registers), warps 4-11 the
+// epilogue (warpgroups 1-2, grown to kRegsEpi): two warps per TMEM lane
+// quadrant (warp w reads lanes 32 (w % 4)..), one taking the even and one
+// the odd 64-column chunks, so an accumulator drains twice as fast as with
+// one warp per quadrant (the drain paces the next unit's first MMAs and the
+// end of the launch).
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 128 + kEpiThreads;
+// setmaxnreg moves registers inside the CTA's pool, i.e. what the launch
+// allocated: 384 threads x 168 (the __launch_bounds__(384, 1) cap) = 64512
+constexpr int kRegsCtl = 56;
+constexpr int kRegsEpi = 224;
+static_assert(128 * kRegsCtl + kEpiThreads * kRegsEpi <= kThreads * (65536 / kThreads / 8 * 8),
+              "the register budgets exceed the CTA's launch allocation (setmaxnreg.inc would never succeed)");
 constexpr int kStages = kLayerStages;
 constexpr int kBlockK = 64;                              // bf16 elements = 128 B swizzle atom
 constexpr uint32_t kSmemA = kTileRows * kBlockK * 2;     // 16 KB: this CTA's 128 A rows
@@ -51,7 +66,7 @@ constexpr uint32_t kTmemCols = kBlockN;                  // 512 = both accumulat
 constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(2 * kTileRows, kHalfN);
 constexpr int kEpiThread0 = 128;                         // first epilogue thread
 constexpr uint32_t kSmemEpiWarp = 32 * 128;              // one warp's 32 rows x 64 columns (bf16)
-constexpr uint32_t kSmemEpi = 2 * 4 * kSmemEpiWarp;      // double-buffered, 4 epilogue warps
+constexpr uint32_t kSmemEpi = kEpiWarps * kSmemEpiWarp;  // one staging buffer per epilogue warp
 // a dispatch CTA's ring + bookkeeping live in the same dynamic smem
 static_assert(comm::kRingBytes + sizeof(comm::CommSmem) <= kStages * kSmemStage + kSmemEpi,
               "dispatch ring and its bookkeeping exceed the layer kernel's shared memory");
@@ -118,10 +133,10 @@ constexpr uint64_t kHelpPollNs = COMET_HELP_POLL_NS;  // split-K: how long an ea
 
 constexpr int kSchedSlots = 2;
 constexpr int kLifeTask = (1 << 20) - 2;  // timeline task id of a CTA's lifetime record
-// Readers of each claimed unit id: leader CTA producer + MMA + 4 epilogue
-// warps, peer CTA producer + 4 epilogue warps (all arrive on the leader's
+// Readers of each claimed unit id: leader CTA producer + MMA + 8 epilogue
+// warps, peer CTA producer + 8 epilogue warps (all arrive on the leader's
 // slot-empty barrier).
-constexpr uint32_t kSchedReaders = 11;
+constexpr uint32_t kSchedReaders = 2 * (1 + kEpiWarps) + 1;
 // The producer asks for its next unit this many k-blocks before the end of
 // the current unit's loads (~4 us of MMA: covers the claim's atomic and
 // broadcast, keeps the claim-ahead short).
@@ -220,8 +235,8 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       ptx::mbar_init(empty + s, 1);
     }
     ptx::mbar_init(tfull, 1);
-    ptx::mbar_init(tempty + 0, 2 * 128);
-    ptx::mbar_init(tempty + 1, 2 * 128);
+    ptx::mbar_init(tempty + 0, 2 * kEpiThreads);
+    ptx::mbar_init(tempty + 1, 2 * kEpiThreads);
     for (int s = 0; s < kSchedSlots; ++s) {
       ptx::mbar_init(sfull + s, 1);
       ptx::mbar_init(sempty + s, kSchedReaders);
@@ -262,6 +277,11 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
     return __shfl_sync(0xffffffffu, g, 0);
   };
 
+  // Registers move from the single-lane control warps (warpgroup 0) to the
+  // epilogue (warpgroups 1-2): each side changes its budget at the top of its
+  // branch (ptxas allocates every region under the budget that dominates it).
+  if (warp < 4) {
+  ptx::setmaxnreg_dec<kRegsCtl>();
   if (warp == 3) {
     // ---------------- scheduler (leader CTA, one thread) ----------------
     // Claims just in time: unit i+1 is claimed when the producer asks for it,
@@ -303,7 +323,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         for (int q = 0; q < 2 * P; ++q)
           if (p.pull_local ? reinterpret_cast<const int4*>(p.pairs)[q >> 1].z > kTileRows * (q & 1)
                            : (reinterpret_cast<const int4*>(p.pairs)[q >> 1].w >> (q & 1)) & 1)
-            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.xg_ready + q), p.epoch)) sp.pause(64, 2); }
+            { ptx::SpinCtl sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(p.xg_ready + q), p.epoch)) sp.pause(64, 2); }
         seq_done = true;
       }
       if (lane == 0) {
@@ -311,7 +331,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (w.layer == 0 && pulled && !COMET_DBG(p.debug, 1)) {
           // this CTA's 128 A rows include rows pulled over NVLink by a dispatch CTA
           const uint32_t* flag = p.xg_ready + (w.pair * 2 + static_cast<int>(cta));
-          { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) sp.pause(32, 3); }
+          { ptx::SpinCtl sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(flag), p.epoch)) sp.pause(32, 3); }
           ptx::fence_async_global();
         }
       }
@@ -332,7 +352,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         if (gate_h && lane == 0 && (kb == kb0 || (kb & (kBlockN / kBlockK - 1)) == 0)) {
           const int nb0 = kb / static_cast<int>(kBlockN / kBlockK);
           const uint32_t target = narrow_block(f.l[0], nb0) ? 1u : 2u;
-          { ptx::Spin sp; while (ptx::ld_acquire_gpu(hc + nb0) < target) sp.pause(32, 4); }
+          { ptx::SpinCtl sp; while (ptx::ld_acquire_gpu(hc + nb0) < target) sp.pause(32, 4); }
           ptx::fence_async_global();
         }
         if (lane == 0 && COMET_DBG(p.debug, 16)) {
@@ -405,9 +425,13 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         tl_record(p, kRoleMma, it, g, t_m, ptx::globaltimer());
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
     // ---------------- epilogue: TMEM -> registers -> global ----------------
-    const int ew = warp - 4;
+    ptx::setmaxnreg_inc<kRegsEpi>();
+    const int ew = warp - 4;       // 0..7
+    const int quad = ew & 3;       // TMEM lane quadrant = output rows 32 quad.. of the CTA's 128
+    const int sub = ew >> 2;       // 0: even 64-column chunks, 1: odd
     for (int it = 0;; ++it) {
       const int g = next_unit(it);
       if (g < 0) break;
@@ -419,7 +443,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       wait(tfull, it & 1);
       ptx::tc_fence_after();
       const uint64_t t_e = ptx::globaltimer();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       const int col0 = w.half > 0 ? static_cast<int>(kHalfN) : 0;  // half unit: its columns
       const int cols_left = p.out_ld - w.nb * kBlockN - col0;      // ragged last n-block (e.g. K/tp = 3200)
       const int n_chunks = w.half < 0 ? static_cast<int>(kBlockN / 64) : static_cast<int>(kHalfN / 64);
@@ -428,7 +452,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // the row of its token's last hosted expert -- the token's weighted sum
       // over its hosted experts (executor.py:102-120), written to y (world 1)
       // or pushed straight into the source rank's combine slot over NVLink.
-      const int my_row = row0 + ew * 32 + lane;
+      const int my_row = row0 + quad * 32 + lane;
       __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN + col0;
       float scale = 1.f;
       int fold_t = -1, fold_s = 0;  // token and own slot of a last-hosted row
@@ -472,7 +496,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           if (pos < 0) continue;
           for (int h = h_lo; h <= h_hi; ++h) {
             const uint32_t* fl = p.tile_done + (static_cast<long long>(pos >> 7) * NB + w.nb) * 2 + h;
-            { ptx::Spin sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) sp.pause(64, 5); }
+            { ptx::SpinEpi sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) sp.pause(64, 5); }
           }
         }
       };
@@ -525,13 +549,13 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // row's 128 B (XOR-swizzled 16 B granules, conflict-free), then each
         // store instruction writes 4 whole 128 B lines (8 lanes per row).
         // Only this warp touches its staging rows: __syncwarp suffices.
-        // (seq: this epilogue's count of processed chunks -- the staging
-        // buffer alternates per processed chunk, not per column chunk)
-        uint8_t* stg = epi_smem + ((seq & 1) * 4 + ew) * kSmemEpiWarp;
-        // TMA store: the staging rows (SW128 layout) of chunk seq-2 must be
-        // read out before they are overwritten
-        if (tma_out && seq >= 2) {
-          if (lane == 0) ptx::bulk_wait_read<1>();
+        // (seq: this warp's count of processed chunks; one staging buffer
+        // per warp -- the quadrant's other warp stores the chunks between)
+        uint8_t* stg = epi_smem + ew * kSmemEpiWarp;
+        // TMA store: the staging rows (SW128 layout) of this warp's previous
+        // chunk must be read out before they are overwritten
+        if (tma_out && seq >= 1) {
+          if (lane == 0) ptx::bulk_wait_read<0>();
           __syncwarp();
         }
         if (COMET_DBG(p.debug, 512)) {  // debug: pack only (no staging, no stores)
@@ -544,14 +568,14 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
               make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         if (COMET_DBG(p.debug, 256)) return;  // debug: staged, not stored
         if (tma_out) {
-          // rows row0+32*ew.. are contiguous in H / yrows: one async 2D tensor
+          // rows row0+32*quad.. are contiguous in H / yrows: one async 2D tensor
           // store of the warp's 32 x 64 block (the swizzled staging layout is
           // the map's SWIZZLE_128B box) instead of 8 transposed st.global
           ptx::fence_async_shared();
           __syncwarp();
           if (lane == 0) {
             ptx::tma_store_2d(w.layer ? tm_s1 : tm_s0, stg, w.nb * static_cast<int>(kBlockN) + col0 + s * 64,
-                              row0 + ew * 32);
+                              row0 + quad * 32);
             ptx::bulk_commit();
           }
           return;
@@ -574,7 +598,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const int S = w.np;
       const long long split_tile = static_cast<long long>(row0 >> 7) * NB + w.nb;
       float4* part_row = S > 1 ? reinterpret_cast<float4*>(p.part + (split_tile * S + w.ks) * kTileRows * kBlockN) +
-                                     ew * 32 + lane
+                                     quad * 32 + lane
                                : nullptr;
       // Split-K finisher.  Two slices (the uneven layer1 tail split, or S = 2
       // split-K): roles are decided when the accumulator is ready -- the
@@ -596,25 +620,27 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       uint32_t split_done = 0u;  // S > 2: the 256-column halves whose last chunk this slice finished
       uint32_t* landed = p.split_cnt + 256 + split_tile;
       const float4* rows0 =
-          S > 1 ? reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + ew * 32 + lane : nullptr;
+          S > 1 ? reinterpret_cast<const float4*>(p.part + split_tile * S * kTileRows * kBlockN) + quad * 32 + lane : nullptr;
       if (early) {
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         if (threadIdx.x == kEpiThread0) *sflag = atomicAdd(p.split_cnt + split_tile, 1u) == 1u;
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         finisher = *reinterpret_cast<volatile int*>(sflag) != 0;
         if (finisher) {
           if (threadIdx.x == kEpiThread0) {
-            ptx::Spin sp;
+            ptx::SpinEpi sp;
             while (ptx::ld_acquire_gpu(landed) < 1u) sp.pause(64, 6);
           }
-          ptx::named_bar_sync(1, 128);
+          ptx::named_bar_sync(1, kEpiThreads);
           __threadfence();
         }
       }
       if (finisher) fold_wait();
+      int seq = 0;
 #pragma unroll 1
-      for (int s = 0; s < n_chunks; ++s) {
-        const bool half_end = (s == kBlockN / 128 - 1) || (s == kBlockN / 64 - 1);
+      for (int s = sub; s < n_chunks; s += 2) {
+        // this warp's last chunk of its accumulator half: release the half
+        const bool half_end = s + 2 >= n_chunks || ((s * 64) / static_cast<int>(kHalfN)) != (((s + 2) * 64) / static_cast<int>(kHalfN));
         if (COMET_DBG(p.debug, 128)) {  // debug: drain nothing
           if (half_end) {
             ptx::tc_fence_before();
@@ -675,7 +701,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
             }
           }
         }
-        process(s, s, v0, v1);
+        process(s, seq++, v0, v1);
       }
       if (tma_out) {  // this warp's tensor stores complete before the unit is counted
         if (lane == 0) ptx::bulk_wait<0>();
@@ -684,7 +710,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       if (early) {
         if (!finisher) {  // partial in memory -> landed
           __threadfence();
-          ptx::named_bar_sync(1, 128);
+          ptx::named_bar_sync(1, kEpiThreads);
           if (threadIdx.x == kEpiThread0) ptx::red_release_gpu_add(landed, 1u);
         } else if (threadIdx.x == kEpiThread0) {  // both slices arrived and landed: reset for the next launch
           p.split_cnt[split_tile] = 0u;
@@ -700,7 +726,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // queued on one pair (consecutive claims of short slices) cannot
         // deadlock.  Every counter is reset by the launch's last CTA out.
         __threadfence();
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         if (threadIdx.x == kEpiThread0) {
           uint32_t* arrive = p.split_cnt + split_tile;
           bool help = ptx::atom_acq_rel_gpu_add(arrive, 1u) == static_cast<uint32_t>(S - 1);
@@ -712,20 +738,28 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           }
           *sflag = help;
         }
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         const bool help = *reinterpret_cast<volatile int*>(sflag) != 0;
-        int mine[2] = {0, 0};  // chunks this CTA finished per 256-column half
+        int mine[2] = {0, 0};  // (kEpiThread0) real chunks this CTA finished per 256-column half
         if (help) {
           __threadfence();
           fold_wait();
           uint32_t* next = p.split_cnt + 256 + split_tile;
-          for (int seq = 0;; ++seq) {
-            ptx::named_bar_sync(1, 128);  // the previous claim was read by every thread
-            if (threadIdx.x == kEpiThread0) *sflag = static_cast<int>(atomicAdd(next, 1u));
-            ptx::named_bar_sync(1, 128);
-            const int s = *reinterpret_cast<volatile int*>(sflag);
-            if (s >= n_chunks) break;
-            if (s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;
+          // two chunks per claim: the even-chunk warps take the first, the
+          // odd-chunk warps the second
+          for (int hseq = 0;; ++hseq) {
+            ptx::named_bar_sync(1, kEpiThreads);  // the previous claim was read by every thread
+            if (threadIdx.x == kEpiThread0) {
+              const int c0 = static_cast<int>(atomicAdd(next, 2u));
+              *sflag = c0;
+              for (int c = c0; c < min(c0 + 2, n_chunks); ++c)
+                if (c * 64 < cols_left) ++mine[w.half >= 0 ? w.half : (c * 64 >= static_cast<int>(kHalfN) ? 1 : 0)];
+            }
+            ptx::named_bar_sync(1, kEpiThreads);
+            const int c0 = *reinterpret_cast<volatile int*>(sflag);
+            if (c0 >= n_chunks) break;
+            const int s = c0 + sub;
+            if (s >= n_chunks || s * 64 >= cols_left || COMET_DBG(p.debug, 64)) continue;
             uint32_t v0[32], v1[32];
             float acc[64];
 #pragma unroll
@@ -743,8 +777,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
               v0[i] = __float_as_uint(acc[i]);
               v1[i] = __float_as_uint(acc[32 + i]);
             }
-            process(s, seq, v0, v1);
-            ++mine[w.half >= 0 ? w.half : (s * 64 >= static_cast<int>(kHalfN) ? 1 : 0)];
+            process(s, seq++, v0, v1);
           }
           if (tma_out) {
             if (lane == 0) ptx::bulk_wait<0>();
@@ -752,7 +785,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           }
         }
         __threadfence();
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         if (threadIdx.x == kEpiThread0) {
           // a half is complete when all of its real chunks are (any CTA)
           uint32_t done = 0u;
@@ -766,7 +799,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           }
           *sflag = static_cast<int>(done);
         }
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         split_done = static_cast<uint32_t>(*reinterpret_cast<volatile int*>(sflag));
       }
       // completion counted in real 256-column halves (half 1 of a narrow last
@@ -781,7 +814,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // this CTA's 128 H rows of the unit's columns are in memory -> count
         // them for the layer1 units that read the tile as their A operand
         ptx::fence_async_global();
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         if (threadIdx.x == kEpiThread0 && amount) {
           __threadfence();
           ptx::red_release_gpu_add(f.h_cnt + static_cast<long long>(row0 >> 7) * NB + w.nb, amount);
@@ -789,12 +822,12 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
         if (p.out_cnt && p.fuse_combine)
-          srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
+          if (sub == 0) srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
         // pushed rows become visible to the peer through the releasing
         // thread's system-scope fence in nb_contributed (cumulative over the
         // CTA's stores ordered before it by the barrier) -- one fence per CTA
         // instead of one per thread
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEpiThreads);
         if (p.out_cnt && p.fuse_combine && threadIdx.x == kEpiThread0 && amount) {
           // streamed forward: these output rows' halves are final -> count
           // them per token chunk (rows are token-sorted: few runs) for the

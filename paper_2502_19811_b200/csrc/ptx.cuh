@@ -211,6 +211,12 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, 
                : "memory");
 }
 
+// Warpgroup register reallocation (every thread of the warpgroup executes it)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(N)); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(N)); }
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -382,12 +388,18 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
 // memory, polled with the clock)
 static __device__ unsigned long long g_spin_timeout_ns = 600ull * 1000 * 1000 * 1000;
 static __device__ const volatile uint32_t* g_abort_flag = nullptr;
-__device__ __noinline__ inline void spin_timeout(int site, bool aborted) {
+// One out-of-line report per register-budget region (R): a noinline function
+// called from regions with different setmaxnreg budgets makes ptxas compile
+// every region under the smallest one, so the layer kernel's control warps
+// (R = 1) and epilogue warps (R = 2) each get their own copy.
+template <int R = 0>
+__device__ __noinline__ void spin_timeout(int site, bool aborted) {
   printf("comet: device wait %s (site %d, block %d, thread %d)\n", aborted ? "aborted by the host" : "timed out",
          site, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));
   __trap();
 }
-struct Spin {
+template <int R = 0>
+struct SpinT {
   unsigned n = 0;
   unsigned long long t0 = 0;
   __device__ __forceinline__ void pause(unsigned ns, int site) {
@@ -397,14 +409,17 @@ struct Spin {
     if (t0 == 0) {
       t0 = t;
     } else if (t - t0 > g_spin_timeout_ns) {
-      spin_timeout(site, false);
+      spin_timeout<R>(site, false);
     }
     // the host abort word lives in pinned host memory: a PCIe read, so it is
     // polled only by waits that already spun for > 1 ms (a straggling peer),
     // never on the microsecond-scale waits of a healthy forward
-    if (t - t0 > 1000000ull && g_abort_flag != nullptr && *g_abort_flag != 0u) spin_timeout(site, true);
+    if (t - t0 > 1000000ull && g_abort_flag != nullptr && *g_abort_flag != 0u) spin_timeout<R>(site, true);
   }
 };
+using Spin = SpinT<0>;
+using SpinCtl = SpinT<1>;  // layer kernel control warps (setmaxnreg.dec region)
+using SpinEpi = SpinT<2>;  // layer kernel epilogue warps (setmaxnreg.inc region)
 
 }  // namespace ptx
 }  // namespace comet
