@@ -201,3 +201,98 @@ class EmulatedGroup:
         for l in self.layers:
             l.close()
         self.layers = []
+
+
+class EmulatedUnfused:
+    """The unfused comparison path (``unfused.UnfusedLayer``: gather,
+    all-to-all, cuBLAS grouped GEMMs, all-to-all back, top-k reduce) for
+    every rank of an ``EmulatedGroup``, on the same GPU, weights and tokens,
+    timed the way the fused group is: each rank's own phases with CUDA
+    events, the all-to-all as the receiving rank's copies of its rows from
+    the senders' buffers (HBM copies: the NVLink transfer of a real
+    deployment is slower), host split-size synchronisation outside the
+    timed intervals (a real ``all_to_all_single`` pays it).  Latency = max
+    over ranks of the rank's summed phases.  ``forward`` returns the rank
+    outputs (checked against the oracle by tests)."""
+
+    def __init__(self, grp: "EmulatedGroup", activation: Optional[str] = None):
+        from .unfused import UnfusedLayer
+        torch = grp.torch
+        self.torch, self.grp = torch, grp
+        self.M = grp.M
+        self.layers = []
+        for r, l in enumerate(grp.layers):
+            w0 = l.weights.w0t.transpose(1, 2).contiguous()  # [E_r, N, K/tp], row-major like the reference
+            w1 = l.weights.w1t.transpose(1, 2).contiguous()  # [E_r, K/tp, N]
+            self.layers.append(UnfusedLayer(grp.model, grp.parallel, r, w0, w1, activation=activation))
+        self.xs = []
+        for l in grp.layers:
+            lo, hi = l.token_range(self.M)
+            self.xs.append(l.ctx.token_buffer()[lo:hi])
+
+    def forward(self, combine_w=None, record: bool = False):
+        torch = self.torch
+        W = self.grp.parallel.world_size
+        M, topk = self.M, self.grp.ex.shape[1]
+        times = [[] for _ in range(W)]
+
+        def timed(r, fn):
+            a = torch.cuda.Event(enable_timing=True) if record else None
+            b = torch.cuda.Event(enable_timing=True) if record else None
+            if a is not None:
+                a.record()
+            out = fn()
+            if b is not None:
+                b.record()
+                times[r].append((a, b))
+            return out
+
+        # 1. per source rank: send order and the gathered rows
+        plans = []
+        for r, ul in enumerate(self.layers):
+            lo, hi = self.grp.layers[r].token_range(M)
+            ex_r = self.grp.ex[lo:hi]
+            plans.append(timed(r, lambda ul=ul, ex_r=ex_r, r=r: (
+                lambda p: (p, self.xs[r][p[1] // topk], p[3].int()))(ul._plan(ex_r))))
+        counts = [p[0][2].tolist() for p in plans]  # split sizes on the host (untimed)
+        offs = [np.concatenate([[0], np.cumsum(c)]) for c in counts]
+        # 2. all-to-all: receiver d copies its rows from every sender
+        recv = []
+        for d in range(W):
+            recv.append(timed(d, lambda d=d: (
+                torch.cat([plans[r][1][offs[r][d]:offs[r][d + 1]] for r in range(W)]),
+                torch.cat([plans[r][2][offs[r][d]:offs[r][d + 1]] for r in range(W)]))))
+        # 3. expert GEMMs on every rank
+        backs = [timed(d, lambda d=d: self.layers[d]._experts(*recv[d])) for d in range(W)]
+        # 4. all-to-all back: source r copies its rows from every expert rank
+        roff = [np.concatenate([[0], np.cumsum([counts[r][d] for r in range(W)])]) for d in range(W)]
+        rets = [timed(r, lambda r=r: torch.cat([backs[d][roff[d][r]:roff[d][r + 1]] for d in range(W)]))
+                for r in range(W)]
+        # 5. top-k (weighted) reduce at the source
+        outs = []
+        for r in range(W):
+            lo, hi = self.grp.layers[r].token_range(M)
+            src_row = plans[r][0][1]
+
+            def red(r=r, lo=lo, hi=hi, src_row=src_row):
+                rows = torch.zeros((hi - lo) * topk, rets[r].shape[1], dtype=torch.float32, device=rets[r].device)
+                rows.index_add_(0, src_row, rets[r].float())
+                rows = rows.view(hi - lo, topk, -1)
+                if combine_w is not None:
+                    rows = rows * combine_w[lo:hi].float().unsqueeze(-1)
+                return rows.sum(1).to(torch.bfloat16)
+            outs.append(timed(r, red))
+        return outs, times
+
+    def measure(self, iters: int = 5, warmup: int = 2) -> Dict[str, object]:
+        torch = self.torch
+        for _ in range(warmup):
+            self.forward()
+        torch.cuda.synchronize()
+        per_iter = []
+        for _ in range(iters):
+            _, times = self.forward(record=True)
+            torch.cuda.synchronize()
+            per_iter.append([sum(a.elapsed_time(b) for a, b in t) for t in times])
+        per_rank = [statistics.median(it[r] for it in per_iter) for r in range(len(per_iter[0]))]
+        return {"latency_ms": max(per_rank), "per_rank_ms": per_rank, "hot_rank": int(np.argmax(per_rank))}

@@ -427,3 +427,41 @@ def test_zerocopy_unweighted_activations(act):
     ref = oracle_bf16_inputs(x.float().numpy(), w.w0, w.w1, routing.as_array(), fns[act])
     assert_close(out.float().numpy(), ref, what=f"zero-copy unweighted act={act}")
     layer.close()
+
+
+@pytest.mark.parametrize("tp,ep,topk", [(1, 2, 2), (2, 2, 3), (1, 4, 8)])
+def test_emulated_unfused_matches_fused(tp, ep, topk):
+    """measure.EmulatedUnfused (the unfused all-to-all + grouped-GEMM path,
+    every rank emulated on this GPU, the comparison baseline of
+    tools/matrix.py at EP > 1) computes the same layer as the fused group:
+    both within tolerance of a torch fp32 reference of the same weights."""
+    import torch
+    from paper_2502_19811_b200.measure import EmulatedGroup, EmulatedUnfused
+    E = 16 if topk == 8 else 8
+    model = ModelConfig(L=1, E=E, topk=topk, N=512, K=1024)
+    par = ParallelSpec(tp, ep)
+    routing = build_routing(model, par, WorkloadSpec(M=1024, seed=81, std=0.032))
+    grp = EmulatedGroup(model, par, routing, knobs=LayerKnobs(n_comm0=8, n_comm1=0))
+    cw = torch.rand(1024, topk, device="cuda", generator=torch.Generator(device="cuda").manual_seed(82))
+    un = EmulatedUnfused(grp)
+    outs, _ = un.forward(combine_w=cw)
+    y_un = torch.cat(outs).float()
+    # fp32 reference from the group's own bf16 weights and tokens
+    x = torch.cat(un.xs).float()
+    ex = grp.ex.long()
+    y_ref = torch.zeros(1024, 512, device="cuda")
+    kl = model.K // tp
+    for r, l in enumerate(grp.layers):
+        e_lo = par.ep_group_of_rank(r) * (E // par.ep)
+        for j in range(E // par.ep):
+            hit = (ex == e_lo + j)
+            t_idx, slot = hit.nonzero(as_tuple=True)
+            if t_idx.numel() == 0:
+                continue
+            h = (x[t_idx] @ l.weights.w0t[j, :kl, :512].float().t()).to(torch.bfloat16).float()
+            yr = (h @ l.weights.w1t[j, :512, :kl].float().t()).to(torch.bfloat16).float()
+            y_ref.index_add_(0, t_idx, yr * cw[t_idx, slot].unsqueeze(1))
+    assert_close(y_un.cpu().numpy(), y_ref.cpu().numpy(), what=f"emulated unfused tp={tp} ep={ep} topk={topk}")
+    lat = un.measure(iters=2, warmup=1)
+    assert lat["latency_ms"] > 0 and len(lat["per_rank_ms"]) == par.world_size
+    grp.close()

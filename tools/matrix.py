@@ -3,7 +3,8 @@
 Every configuration runs the full fused forward with all EP x TP ranks
 emulated on this GPU (paper_2502_19811_b200.measure.EmulatedGroup): latency =
 max over ranks of the rank's kernel-time sum.  EP=1 rows are real
-single-GPU forwards and also time the unfused cuBLAS grouped-GEMM path.
+single-GPU forwards.  Every row also times the unfused all-to-all + cuBLAS
+grouped-GEMM path (EP > 1: measure.EmulatedUnfused, the same emulation).
 Roofline per §8(d) at the measured burst and sustained bf16 peaks.
 
     python tools/matrix.py [--quick] [--out gpurun_out/matrix.jsonl]
@@ -120,13 +121,17 @@ def main():
                    "pct_roofline_sustained": round(100 * rf_s.ms / best["latency_ms"], 1),
                    "peaks": {"burst_tflops": burst, "sustained_tflops": sust, "source": src}}
             rec.update(extra_terms(routing, rec["latency_ms"], hbm))
-            if par.world_size == 1:
-                try:
+            try:
+                if par.world_size == 1:
                     u = unfused_ms(grp)
-                    rec["unfused_ms"] = round(u, 4)
-                    rec["speedup_vs_unfused"] = round(u / best["latency_ms"], 3)
-                except Exception as exc:  # report, keep going
-                    rec["unfused_error"] = repr(exc)[:200]
+                else:  # every rank emulated: all-to-alls as HBM copies (measure.EmulatedUnfused)
+                    from paper_2502_19811_b200.measure import EmulatedUnfused
+                    u = EmulatedUnfused(grp).measure(iters=a.iters)["latency_ms"]
+                    torch.cuda.empty_cache()
+                rec["unfused_ms"] = round(u, 4)
+                rec["speedup_vs_unfused"] = round(u / best["latency_ms"], 3)
+            except Exception as exc:  # report, keep going
+                rec["unfused_error"] = repr(exc)[:200]
             grp.close()
             del grp
             torch.cuda.empty_cache()
