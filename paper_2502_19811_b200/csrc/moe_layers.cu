@@ -489,7 +489,9 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // earlier hosted rows live in units claimed before this one (same
       // n-block columns, lower sequence index): wait for their tiles
       auto fold_wait = [&]() {
-        if (fold_t < 0) return;
+        // (a split-tail half 1 of a narrow last n-block has no real columns:
+        // nothing to fold, and its predecessors never publish that half)
+        if (fold_t < 0 || cols_left <= 0) return;
         for (int s2 = 0; s2 < p.topk; ++s2) {
           if (s2 == fold_s) continue;
           const int pos = p.tok_pos[fold_t * p.topk + s2];
