@@ -179,7 +179,7 @@ def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSp
                 stride: int = 2, rank: int = 0, max_nc: int = 16, repeats: int = 5,
                 measure: Optional[Callable[..., float]] = None,
                 candidates: Optional[Sequence[int]] = None,
-                groups: Optional[Sequence[int]] = None) -> SplitRecord:
+                groups: Optional[Sequence[int]] = None, passes: int = 1) -> SplitRecord:
     """Measure the fused layer at each candidate n_c and record the argmin.
 
     ``measure(n_c) -> seconds`` defaults to timing the layer on this GPU with
@@ -191,7 +191,9 @@ def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSp
     accepted for signature compatibility with the reference and ignored.
     ``groups`` (B200 extension): layer0 pair-group sizes swept jointly with
     n_c (``measure(n_c, group0)``); the record keeps the curve of the best
-    group and that group in ``group0``.
+    group and that group in ``group0``.  ``passes`` > 1 measures the whole
+    grid that many times round-robin and keeps each point's minimum (robust
+    to slow drift of the clock between points of a flat curve).
     """
     if blocks is None:
         from . import _lib
@@ -201,9 +203,15 @@ def sweep_split(model: ModelConfig, parallel: ParallelSpec, workload: WorkloadSp
     cands = list(candidates) if candidates is not None else candidate_ncs(blocks, stride, max_nc)
     key = SplitKey.for_config(model, parallel, workload.M, cost_name, blocks)
     if not groups:
-        points = [(nc, int(round(measure(nc) * 1e9))) for nc in cands]
-        return record_from_curve(key, points)
-    curves = {g: [(nc, int(round(measure(nc, g) * 1e9))) for nc in cands] for g in groups}
+        lat = {nc: min(measure(nc) for _ in range(max(1, passes))) for nc in cands}
+        return record_from_curve(key, [(nc, int(round(lat[nc] * 1e9))) for nc in cands])
+    lat = {}
+    for _ in range(max(1, passes)):
+        for g in groups:
+            for nc in cands:
+                t = measure(nc, g)
+                lat[(g, nc)] = min(t, lat.get((g, nc), t))
+    curves = {g: [(nc, int(round(lat[(g, nc)] * 1e9))) for nc in cands] for g in groups}
     best = min(groups, key=lambda g: (min(ns for _, ns in curves[g]), g))
     return record_from_curve(key, curves[best], group0=best)
 

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "paper_2502_19811_b200", "split_b200.json"))
     ap.add_argument("--repeats", type=int, default=5)
+    ap.add_argument("--passes", type=int, default=3, help="round-robin passes over the grid, minimum per point")
     a = ap.parse_args()
     meta = SplitMetadata(records=[])
     for shape, ep, tp, M in configs(a.quick):
@@ -52,7 +53,8 @@ def main():
         model = ModelConfig(L=1, E=E, topk=topk, N=N, K=K)
         t0 = time.time()
         rec = sweep_split(model, ParallelSpec(tp=tp, ep=ep), WorkloadSpec(M=M, seed=0, std=0.0),
-                          cost_name="b200", candidates=CANDIDATES, repeats=a.repeats, groups=GROUPS)
+                          cost_name="b200", candidates=CANDIDATES, repeats=a.repeats, groups=GROUPS,
+                          passes=a.passes)
         meta.add(rec)
         torch.cuda.empty_cache()
         print(json.dumps({"shape": shape, "ep": ep, "tp": tp, "M": M, "optimal_nc": rec.optimal_nc,
