@@ -105,3 +105,20 @@ def test_joint_group_sweep_and_record_round_trip():
     assert "group0" not in plain.to_json_dict()
     split, src, g0 = choose_knobs(MX, ParallelSpec(1, 8), 8192, 148, SplitMetadata(records=[plain]))
     assert (split.n_c, g0) == (4, default_group0(8))
+
+
+def test_sweep_passes_keep_each_points_minimum():
+    """passes > 1: the grid is measured round-robin and each point keeps its
+    minimum (a drifting clock between the points of a flat curve)."""
+    calls = []
+    noisy = {(2, 4): [900, 700], (4, 4): [800, 800], (2, 8): [850, 860], (4, 8): [990, 600]}
+
+    def measure(nc, g):
+        i = sum(1 for c in calls if c == (nc, g))
+        calls.append((nc, g))
+        return noisy[(nc, g)][i] * 1e-9
+    rec = sweep_split(MX, ParallelSpec(1, 8), WorkloadSpec(M=8192), blocks=148, candidates=[2, 4],
+                      groups=[4, 8], passes=2, measure=measure)
+    assert (rec.group0, rec.optimal_nc, rec.latency_ns) == (8, 4, 600)
+    assert rec.curve == ((2, 850), (4, 600))
+    assert calls[:4] == [(2, 4), (4, 4), (2, 8), (4, 8)]  # round robin over the grid

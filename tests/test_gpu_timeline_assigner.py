@@ -120,8 +120,11 @@ def test_layer_takes_n_c_from_the_chooser():
         nc, got_src = layer.split_choice(M)
         assert got_src == src
         assert nc == choose_split(model, par, M, sms)[0].n_c
-        layer.knobs = LayerKnobs.for_world(par.world_size, n_comm0=6)
-        assert layer.split_choice(M) == (6, "knob")
+        # the layer0 pair group measured with that n_c (default rule without a record)
+        from paper_2502_19811_b200.assigner import choose_knobs
+        assert layer.group0(M) == choose_knobs(model, par, M, sms)[2]
+        layer.knobs = LayerKnobs.for_world(par.world_size, n_comm0=6, group0=3)
+        assert layer.split_choice(M) == (6, "knob") and layer.group0(M) == 3
         layer.close()
     w1 = RankWeights(torch.zeros(8, 1024, 512, dtype=torch.bfloat16, device="cuda"),
                      torch.zeros(8, 512, 1024, dtype=torch.bfloat16, device="cuda"))
