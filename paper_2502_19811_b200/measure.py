@@ -193,9 +193,23 @@ class EmulatedGroup:
         med = {k: [statistics.median(it[k][r] for it in per_iter) for r in range(W)] for k in per_iter[0]}
         per_rank = [sum(med[k][r] for k in med) for r in range(W)]
         hot = int(np.argmax(per_rank))
+        # the same forwards without events between the kernels (PDL chains
+        # intact): whole phase-ordered forward / ranks -- a mean over ranks,
+        # so it hides imbalance; the per-rank event sums above pay ~4 us of
+        # broken launch overlap per kernel boundary (reported alongside)
+        whole = []
+        for _ in range(max(3, iters // 2)):
+            torch.cuda._sleep(3_000_000)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            self._forward_timed(False)
+            b.record()
+            torch.cuda.synchronize()
+            whole.append(a.elapsed_time(b))
         return {"latency_ms": max(per_rank), "hot_rank": hot, "per_rank_ms": per_rank,
                 "kernels_ms_hot_rank": {k: med[k][hot] for k in med},
-                "kernels_ms_max": {k: max(med[k]) for k in med}}
+                "kernels_ms_max": {k: max(med[k]) for k in med},
+                "chained_mean_ms": statistics.median(whole) / W}
 
     def close(self) -> None:
         for l in self.layers:

@@ -114,6 +114,7 @@ def main():
             rec = {"knobs": a.knobs, "shape": shape, "E": E, "topk": topk, "N": N, "K": K, "ep": ep, "tp": tp, "M": M, "std": std,
                    "emulated": par.world_size > 1, "latency_ms": round(best["latency_ms"], 4),
                    "hot_rank": best["hot_rank"], "n_comm0": best["n_comm0"],
+                   "chained_mean_ms": round(best.get("chained_mean_ms", 0.0), 4),
                    "kernels_ms_hot_rank": {k: round(v, 4) for k, v in best["kernels_ms_hot_rank"].items()},
                    "roofline_ms_burst": round(rf_b.ms, 4), "roofline_ms_sustained": round(rf_s.ms, 4),
                    "roofline_bound": rf_b.bound, "t_nvlink_ms": round(rf_b.t_nvlink_ms, 4),
