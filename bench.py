@@ -427,7 +427,7 @@ def run_ours(args):
     t_flops_sust_ms = flops_step / (peak_sust * 1e12) * 1e3
     flops_launch = 2 * (2.0 * rows * N * kl)  # this rank's launch(es) of one step
     achieved_tf = flops_launch / (t_kernel_local * 1e-3) / 1e12
-    traffic = load_traffic("layers" if fused else "layer1")
+    traffic = load_traffic(world, "layers" if fused else "layer1")
     bytes_step = comm_bytes(routing, par, rank, N)
     launches_per_step = (4 if fused else 5) - (0 if (world == 1 and knobs.n_comm1 == 0) else 1) + \
         (1 if world > 1 else 0)
@@ -516,14 +516,17 @@ def comm_bytes(routing, par, rank, N):
             "t_nvlink_ms": round(float(byts.max()) / (nvl * 1e9) * 1e3, 4)}
 
 
-def load_traffic(dominant):
+def load_traffic(world, dominant="layers"):
     """dram read+write bytes per launch of the dominant kernel from the
-    committed ncu --set full summary (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_layer_summary.json")
+    committed ncu --set full capture of the same configuration (profiles/:
+    the N=1 workload's layer kernel; Mixtral EP=8 rank 0 for N=8), or None
+    when no capture of this configuration is committed."""
+    name = {1: "r2_final/ncu_layer_ep1.json", 8: "r2_final/ncu_layer_MX_ep8_tp1.json"}.get(world)
+    if name is None or dominant != "layers":
+        return None
     try:
-        with open(path) as fh:
-            data = json.load(fh)
-        return data[dominant]["dram_bytes"]
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)["layers"]["dram_bytes"]
     except Exception:
         return None
 
