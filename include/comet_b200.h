@@ -242,7 +242,8 @@ int comet_device_info(int device, int32_t out[4]);
  *                  level computation costs the index build 8-12 us and
  *                  PH EP4xTP2 ran 0.300 vs 0.282 ms, QW EP8 0.381 vs 0.376)
  *   GROUP1         layer1 pair-group size, 0 = layer0's group (0)
- *   CHUNK_ROWS     dispatch item rows 1..32 (32)
+ *   CHUNK_ROWS     dispatch item rows 1..32; 0 = auto, ~one item per
+ *                  dispatch CTA for M*topk/ep rows, clamped to 4..32 (0)
  *   PDL            programmatic dependent launch bitmask: 1 local dispatch,
  *                  2 layer kernel, 4 combine kernels, 8 index build (14)
  *   GRID           cap on the persistent grid in CTAs, 0 = every SM (0)

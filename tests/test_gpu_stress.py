@@ -41,7 +41,7 @@ def _case(seed):
     knobs = dict(n_comm0=int(r.choice([2, 4, 8, 16, 32])), n_comm1=0, group0=int(r.choice([1, 2, 4, 8, 16])),
                  ksplit_max=int(r.choice([0, 2, 3, 8])), split1=int(r.choice([-1, 0, 8, 74])),
                  fused=bool(r.integers(0, 4) > 0), streamk=bool(r.integers(0, 4) == 0),
-                 wave1=int(r.choice([1, 2, 4, 8])), chunk_rows=int(r.choice([1, 7, 16, 32])),
+                 wave1=int(r.choice([1, 2, 4, 8])), chunk_rows=int(r.choice([0, 1, 7, 16, 32])),
                  dedup=int(r.integers(0, 4) == 0), fold_order=bool(r.integers(0, 3) == 0),
                  pull_local=bool(r.integers(0, 4) > 0), group1=int(r.choice([0, 0, 1, 4])))
     return E, topk, tp, ep, N, K, M, std, act, weighted, knobs
