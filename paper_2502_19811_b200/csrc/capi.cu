@@ -393,6 +393,7 @@ int comet_ctx_create(const comet_config* cfg, comet_ctx** out) {
       b += align_up(p.n * 4, 256);
     }
     ix.done = reinterpret_cast<uint32_t*>(b);
+    ix.p1_done = reinterpret_cast<uint32_t*>(b + 128);
   }
   ix.cap_rows = x->cap_rows;
   ix.cap_rows_pad = x->cap_rows_pad;
@@ -624,7 +625,8 @@ int comet_index_build_ex(comet_ctx* x, const int32_t* d_experts, int M, int tile
   ix.tpt = std::max(1, (M + 16 * kIndexThreads - 1) / (16 * kIndexThreads));
   const int chunks = (M + kIndexThreads * ix.tpt - 1) / (kIndexThreads * ix.tpt);
   if (chunks > kIndexMaxChunks) return fail(COMET_EINVAL, "M=%d too large for the index build", M);
-  const int grid = std::min(x->n_sm, std::max(32, x->E_r * chunks));
+  // item CTAs [0, grid - 1) + the table CTA (grid - 1, no items)
+  const int grid = std::min(x->n_sm, std::max(32, x->E_r * chunks + 1));
   // global histogram + transfer matrix accumulate by atomics: zero both (adjacent)
   const size_t zbytes = reinterpret_cast<char*>(x->ix.transfer + c.world * c.world) - reinterpret_cast<char*>(x->ix.counts);
   if (flags & kIndexRefLists) CK(cudaMemsetAsync(x->ix.counts, 0, zbytes, static_cast<cudaStream_t>(stream)));

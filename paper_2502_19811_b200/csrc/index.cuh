@@ -75,7 +75,8 @@ struct IndexDev {
   int32_t* meta;        // [kMetaSlots]
   // scratch
   int32_t* pair_key;    // [P_cap]
-  uint32_t* done;       // [1] CTA completion counter (self-resetting)
+  uint32_t* done;       // [1] item-CTA completion counter (kIndexStream; self-resetting)
+  uint32_t* p1_done;    // [1] fold-mask completion counter (kIndexFoldOrder; self-resetting)
   int32_t* chunk_cnt;   // [E_r * kIndexMaxChunks] hits per (hosted expert, token chunk)
   int32_t* chunk_loc;   // [E_r * kIndexMaxChunks] local-token hits per (hosted expert, chunk)
   uint32_t* chunk_flag; // [E_r * kIndexMaxChunks] build epoch when the item's counts landed (look-back)

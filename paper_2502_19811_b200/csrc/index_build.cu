@@ -14,11 +14,17 @@
 // (hosted expert, token chunk), block-wide ballot scans, no sort.
 //
 // One launch: every CTA writes its token slice's non-hosted slots (and the
-// reference counts / transfer matrix when asked); each item counts its hits,
-// publishes them and looks back at the earlier items (decoupled look-back:
-// the rows before it, no grid barrier), then writes its rows; the last CTA to
-// finish (grid-wide completion counter) builds the tile lists, the 2-CTA
-// pair tables and the combine token list.
+// reference counts / transfer matrix when asked); the item CTAs count each
+// item's hits, publish them and look back at the earlier items (decoupled
+// look-back: the rows before it, no grid barrier), then write its rows.  The
+// last CTA has no items: it sums the items' published hit counts into each
+// hosted expert's totals and builds the tile lists, the 2-CTA pair tables and
+// the combine token list -- they need only those totals -- while the items
+// look back and write their rows.  The tables are the build's longest serial stretch (~7 us,
+// mostly first-touch instruction and constant fetch: the pair-table block
+// takes 3.1 us the first time and 0.65 us when repeated in one launch), so
+// overlapping them with the items instead of following a grid-wide
+// completion count shortens the build.
 #include <climits>
 #include <cstdint>
 
@@ -210,9 +216,14 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     __syncthreads();
     for (int j = tid; j < Er; j += kThreads) ix.fold_part[static_cast<long long>(blockIdx.x) * Er + j] = s_pred[j];
     __syncthreads();
+    // the table CTA reads every slice's masks: the CTA barrier orders the
+    // writes before thread 0's release (cumulative)
+    if (tid == 0) ptx::red_release_gpu_add(ix.p1_done, 1u);
   }
 
   probe(1);
+  const bool table_cta = blockIdx.x == gridDim.x - 1;
+  const int n_item_ctas = gridDim.x - 1;
 
   // -------- rows: one pass per (hosted expert, token chunk) item.  Count the
   // item's hits, publish the counts (epoch flag), look back at every earlier
@@ -220,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   // before this chunk -- a decoupled look-back, no grid barrier: every item
   // waits only on lower items, so the lowest unfinished one never waits),
   // then write the rows: a stable compaction of the rotated token order --------
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  for (int it = table_cta ? items : static_cast<int>(blockIdx.x); it < items; it += n_item_ctas) {
     const int j = it / C, c = it - (it / C) * C, e = ix.e_lo + j;
     int loc;
     uint64_t hit = chunk_hits(ix, c, T, TPT, e, start, n_own, &loc);
@@ -293,30 +304,36 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   }
 
   probe(3);
-  // -------- grid completion: the last CTA builds the schedules --------
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(ix.done, 1u);
-    s_misc[1] = (prev == gridDim.x - 1) ? 1 : 0;
+  if (!table_cta) {
+    if (ix.flags & kIndexStream) {  // the stream pass below reads every item's tok_pos
+      __syncthreads();
+      if (tid == 0) ptx::red_release_gpu_add(ix.done, 1u);
+    }
+    return;
   }
-  __syncthreads();
-  if (!s_misc[1]) return;
-  __threadfence();
-  probe(4);
-  // every item landed: expert totals, row / padded offsets, local prefixes
+  // -------- the table CTA: expert totals (all rows, rows of this rank's
+  // tokens) from the items' published counts (each item publishes them before
+  // its look-back and row writes), then the schedules --------
   __shared__ int s_nloc[kMaxExperts];
   for (int j = tid; j < Er; j += kThreads) {
-    int t = 0, nl = 0;
-    for (int c = 0; c < C; ++c) {
-      t += __ldcg(ix.chunk_cnt + j * C + c);
-      nl += __ldcg(ix.chunk_loc + j * C + c);
-    }
-    s_cnt[j] = t;
-    s_nloc[j] = nl;
-    ix.n_local[j] = nl;
+    s_cnt[j] = 0;
+    s_nloc[j] = 0;
   }
   __syncthreads();
+  for (int q = tid; q < items; q += kThreads) {
+    { ptx::Spin sp; while (ptx::ld_acquire_gpu(ix.chunk_flag + q) != ix.epoch) sp.pause(32, 13); }
+    const int n = __ldcg(ix.chunk_cnt + q), l = __ldcg(ix.chunk_loc + q);
+    if (n) atomicAdd(s_cnt + q / C, n);
+    if (l) atomicAdd(s_nloc + q / C, l);
+  }
+  if ((ix.flags & kIndexFoldOrder) && tid == 0) {  // every slice's fold masks
+    ptx::Spin sp;
+    while (ptx::ld_acquire_gpu(ix.p1_done) < gridDim.x) sp.pause(32, 14);
+    *ix.p1_done = 0u;  // nothing else reads it this launch; ready for the next
+  }
+  __syncthreads();
+  probe(4);
+  for (int j = tid; j < Er; j += kThreads) ix.n_local[j] = s_nloc[j];
   if (tid == 0) {
     int o = 0, pd = 0;
     for (int j = 0; j < Er; ++j) {
@@ -547,6 +564,14 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
   // ---- streamed forward: the fused-combine folder of each token is its
   // hosted row in the LATEST (row tile, expert) pair -- every other row it
   // folds is claimed earlier, so fold waits never point forward ----
+  if (ix.flags & kIndexStream) {  // every item CTA's rows (tok_pos) are in place
+    if (tid == 0) {
+      ptx::Spin sp;
+      while (ptx::ld_acquire_gpu(ix.done) < gridDim.x - 1) sp.pause(32, 15);
+      *ix.done = 0u;
+    }
+    __syncthreads();
+  }
   if ((ix.flags & kIndexStream) && !ovf) {
     for (int t = tid; t < M; t += kThreads) {
       const int32_t* trow = ix.experts + static_cast<long long>(t) * K;
@@ -607,7 +632,6 @@ __global__ void __launch_bounds__(kThreads, 1) index_build_kernel(IndexDev ix) {
     ix.meta[kMetaChunks] = NCH;
     ix.meta[kMetaCombineTok] = s_misc[3];
     ix.meta[kMetaSlots - 1] = (ovf ? 1 : 0) | (ovf1 ? 2 : 0);
-    *ix.done = 0u;  // self-reset for the next launch
   }
 }
 
