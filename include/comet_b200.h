@@ -263,7 +263,15 @@ int comet_device_info(int device, int32_t out[4]);
  *   STREAMK        1: layer1's single partial round (pairs/2 < tiles < pairs,
  *                  no fold chains) as head / tail K slices, the tails
  *                  filling the idle pairs (sched.cuh; measured no faster
- *                  than whole units at Mixtral EP=8 -- kept opt-in; 0) */
+ *                  than whole units at Mixtral EP=8 -- kept opt-in; 0)
+ *   FOLD_STRIDE    fused combine: 0 = the token's last hosted row folds all
+ *                  its other hosted rows; k >= 2 = chained folds -- every
+ *                  k-th hosted row (and the last) folds the rows since the
+ *                  previous folder plus that folder's weighted partial, so
+ *                  a top-8 folder reads <= k rows instead of 7 (measured
+ *                  slower: the intermediate folders' waits cost more than
+ *                  the shorter last folds save, QW EP=8 0.360 -> 0.366 ms at
+ *                  k = 2; 0) */
 #define COMET_OPT_FUSED 0
 #define COMET_OPT_KSPLIT_MAX 1
 #define COMET_OPT_SPLIT_TAIL0 2
@@ -285,7 +293,8 @@ int comet_device_info(int device, int32_t out[4]);
 #define COMET_OPT_STREAM_FUSE 18
 #define COMET_OPT_SEQUENTIAL 19
 #define COMET_OPT_STREAMK 20
-#define COMET_OPT_COUNT 21
+#define COMET_OPT_FOLD_STRIDE 21
+#define COMET_OPT_COUNT 22
 #define COMET_OPT_DEFAULT (-2147483647 - 1)
 int comet_set_option(comet_ctx* ctx, int opt, int value);
 int comet_get_option(comet_ctx* ctx, int opt, int* value);

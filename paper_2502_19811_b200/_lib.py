@@ -42,7 +42,7 @@ OPTIONS = {
     "fused": 0, "ksplit_max": 1, "split_tail0": 2, "split1": 3, "dedup": 4, "pull_local": 5, "fold_order": 6,
     "group1": 7, "chunk_rows": 8, "pdl": 9, "grid": 10, "fuse1": 11, "spin_timeout_ms": 12, "zc_dedup": 13,
     "zc_interleave": 14, "zc_download": 15, "zc_order": 16, "zc_fold_order": 17, "stream_fuse": 18, "sequential": 19,
-    "streamk": 20,
+    "streamk": 20, "fold_stride": 21,
 }
 OPT_DEFAULT = -2147483648
 ROLES = ("load", "mma", "tmem_wait", "epilogue", "comm")

@@ -76,7 +76,7 @@ constexpr int kOptDefaults[COMET_OPT_COUNT] = {
     /*FUSED*/ 1, /*KSPLIT_MAX*/ 8, /*SPLIT_TAIL0*/ 1, /*SPLIT1*/ -1, /*DEDUP*/ -1, /*PULL_LOCAL*/ 1,
     /*FOLD_ORDER*/ 0, /*GROUP1*/ 0, /*CHUNK_ROWS*/ 0, /*PDL*/ 14, /*GRID*/ 0, /*FUSE1*/ 0,
     /*SPIN_TIMEOUT_MS*/ COMET_DEFAULT_SPIN_MS, /*ZC_DEDUP*/ 1, /*ZC_INTERLEAVE*/ 1, /*ZC_DOWNLOAD*/ 8, /*ZC_ORDER*/ 0,
-    /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0, /*STREAMK*/ 0};
+    /*ZC_FOLD_ORDER*/ 0, /*STREAM_FUSE*/ 0, /*SEQUENTIAL*/ 0, /*STREAMK*/ 0, /*FOLD_STRIDE*/ 0};
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous one drains; it calls griddepcontrol.wait before touching
@@ -242,6 +242,8 @@ int comet_set_option(comet_ctx* x, int opt, int value) {
   if (value == COMET_OPT_DEFAULT) value = kOptDefaults[opt];
   if (opt == COMET_OPT_CHUNK_ROWS && (value < 0 || value > 32))
     return fail(COMET_EINVAL, "CHUNK_ROWS must be 0 (auto) or in [1, 32], got %d", value);
+  if (opt == COMET_OPT_FOLD_STRIDE && (value < 0 || value == 1 || value > 8))
+    return fail(COMET_EINVAL, "FOLD_STRIDE must be 0 or in [2, 8], got %d", value);
   if (opt == COMET_OPT_KSPLIT_MAX && (value < 0 || value > 8))
     return fail(COMET_EINVAL, "KSPLIT_MAX must be in [0, 8], got %d", value);
   if (opt == COMET_OPT_GRID && (value < 0 || value == 1 || (value & 1)))
@@ -892,6 +894,7 @@ static int layer1_args(comet_ctx* x, const void* w1t, const float* combine_w, vo
   // local combine kernel reduce yrows.  At world 1 the fold's tile waits cost
   // what the local combine kernel saves (A/B in DESIGN.md), so it is opt-in.
   a.fuse_combine = c.world > 1 || (n_comm == 0 && x->opt[COMET_OPT_FUSE1] != 0);
+  a.fold_stride = x->opt[COMET_OPT_FOLD_STRIDE];
   a.tile_done = x->tile_done;
   if (c.world > 1 || !alone) n_comm = 0;  // combine CTAs only in a layer1-alone launch at world 1
   const int grid = layer_grid(x);
@@ -1157,6 +1160,7 @@ int comet_forward_host(comet_ctx* x, const void* h_x, const int32_t* h_experts, 
   const bool fold = x->opt[COMET_OPT_STREAM_FUSE] != 0;
   f.l[0].stream_combine = fold ? 0 : 1;
   f.l[1].fuse_combine = fold ? 1 : 0;
+  f.l[1].fold_stride = 0;  // the folder is the row claimed last, not the last slot: fold everything there
   f.l[1].publish_tiles = 1;
   f.l[1].y_local = x->y_stream;
   f.l[1].out_cnt = x->counters + 2 * x->nb1;

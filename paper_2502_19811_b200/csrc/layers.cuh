@@ -87,6 +87,8 @@ struct LayerArgs {
   const int32_t* row_widx;    // [Rpad] t * topk + slot of each padded row
   int fuse_combine;           // layer1: the epilogue of each token's last hosted row folds the
                               // earlier rows in and writes y (world 1) / pushes to the source rank
+  int fold_stride;            // fused combine: 0 = that row folds all of them; k >= 2 = chained
+                              // (COMET_OPT_FOLD_STRIDE): hosted rows c % k == k-1 fold too
   uint32_t* tile_done;        // [Rpad/128 * n_blocks * 2] epoch when a 128-row tile's yrows of a 256-column
                               // half of an n-block landed
   const float* combine_w;     // [M*topk] or null

@@ -455,49 +455,71 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const int my_row = row0 + quad * 32 + lane;
       __nv_bfloat16* my_dst = p.out + static_cast<long long>(my_row) * p.out_ld + w.nb * kBlockN + col0;
       float scale = 1.f;
-      int fold_t = -1, fold_s = 0;  // token and own slot of a last-hosted row
-      int nf = 0;                   // earlier hosted rows to fold, their rows and weights
+      int fold_t = -1;              // token of a folding row
+      bool out_row = false;         // this row writes / pushes its token's final sum
+      int nf = 0;                   // rows to fold in, their rows and weights (ascending slot)
       int fpos[kMaxFold];
       float fw[kMaxFold];
       if (w.layer == 1 && p.fuse_combine) {
         const int rd = p.row_dst[my_row];
-        if (rd >= 0) {
-          __nv_bfloat16* base = p.world > 1 ? p.cb_peer[rd >> 24] : p.y_local;
-          my_dst = base + static_cast<long long>(rd & 0xFFFFFF) * p.n_embed + w.nb * kBlockN + col0;
+        const bool real_row = kTileRows * static_cast<int>(cta) + quad * 32 + lane < pr.z;
+        if (rd >= 0 || (p.fold_stride >= 2 && real_row)) {
           const int widx = p.row_widx[my_row];
-          fold_t = widx / p.topk;
-          fold_s = widx - fold_t * p.topk;
-          if (p.combine_w) scale = p.combine_w[widx];
-          // every other hosted row of the token (only earlier slots unless the
-          // streamed forward picked a non-last folder), ascending slot
+          const int t = widx / p.topk, me = widx - t * p.topk;
+          // chained folds (fold_stride k): hosted rows in ascending slot order
+          // form a chain; rows whose chain index c has c % k == k-1, and the
+          // last one, fold the rows since the previous folder (weighted) plus
+          // that folder's row (already a weighted partial, weight 1); the
+          // intermediate folders write their partial to their own yrows row.
+          // k = 0: the last hosted row folds every other hosted row.
+          const int k = p.fold_stride;
+          int c = 0;
+          if (k >= 2)
+            for (int s2 = 0; s2 < me; ++s2) c += p.tok_pos[t * p.topk + s2] >= 0;
+          if (rd >= 0 || c % k == k - 1) {
+            out_row = rd >= 0;
+            if (out_row) {
+              __nv_bfloat16* base = p.world > 1 ? p.cb_peer[rd >> 24] : p.y_local;
+              my_dst = base + static_cast<long long>(rd & 0xFFFFFF) * p.n_embed + w.nb * kBlockN + col0;
+            }
+            fold_t = t;
+            if (p.combine_w) scale = p.combine_w[widx];
+            const int g0 = k >= 2 ? c - c % k : 0;  // chain index of this folder's first own-group row
+            // the rows to fold, ascending slot (k = 0: every other hosted row
+            // -- only earlier slots unless the streamed forward picked a
+            // non-last folder)
+            int ci = 0;  // chain index of slot s2
 #pragma unroll
-          for (int s2 = 0; s2 < kMaxFold + 1; ++s2) {
-            if (s2 >= p.topk) break;
-            if (s2 == fold_s) continue;
-            const int pos = p.tok_pos[fold_t * p.topk + s2];
-            if (pos < 0) continue;
+            for (int s2 = 0; s2 < kMaxFold + 1; ++s2) {
+              if (s2 >= p.topk) break;
+              const int pos = p.tok_pos[t * p.topk + s2];
+              if (pos < 0) continue;
+              const int cs = ci++;
+              if (s2 == me) continue;
+              const bool prev_folder = k >= 2 && cs == g0 - 1;
+              if (k >= 2 && (s2 > me || (cs < g0 && !prev_folder))) continue;
 #pragma unroll
-            for (int j = 0; j < kMaxFold; ++j)  // static register indexing
-              if (j == nf) {
-                fpos[j] = pos;
-                fw[j] = p.combine_w ? p.combine_w[fold_t * p.topk + s2] : 1.f;
-              }
-            ++nf;
+              for (int j = 0; j < kMaxFold; ++j)  // static register indexing
+                if (j == nf) {
+                  fpos[j] = pos;
+                  fw[j] = prev_folder ? 1.f : (p.combine_w ? p.combine_w[t * p.topk + s2] : 1.f);
+                }
+              ++nf;
+            }
           }
         }
       }
-      // earlier hosted rows live in units claimed before this one (same
+      // the rows this one folds live in units claimed before this one (same
       // n-block columns, lower sequence index): wait for their tiles
       auto fold_wait = [&]() {
         // (a split-tail half 1 of a narrow last n-block has no real columns:
         // nothing to fold, and its predecessors never publish that half)
         if (fold_t < 0 || cols_left <= 0) return;
-        for (int s2 = 0; s2 < p.topk; ++s2) {
-          if (s2 == fold_s) continue;
-          const int pos = p.tok_pos[fold_t * p.topk + s2];
-          if (pos < 0) continue;
+#pragma unroll
+        for (int j = 0; j < kMaxFold; ++j) {
+          if (j >= nf) break;
           for (int h = h_lo; h <= h_hi; ++h) {
-            const uint32_t* fl = p.tile_done + (static_cast<long long>(pos >> 7) * NB + w.nb) * 2 + h;
+            const uint32_t* fl = p.tile_done + (static_cast<long long>(fpos[j] >> 7) * NB + w.nb) * 2 + h;
             { ptx::SpinEpi sp; while (!ptx::epoch_reached(ptx::ld_acquire_gpu(fl), p.epoch)) sp.pause(64, 5); }
           }
         }
@@ -824,7 +846,7 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       } else if (w.layer == 1) {
         // this CTA's 128 rows of column block nb are in memory -> count them
         if (p.out_cnt && p.fuse_combine)
-          if (sub == 0) srow_chunk[threadIdx.x - kEpiThread0] = (fold_t >= 0 && amount) ? fold_t / p.chunk_tokens : -1;
+          if (sub == 0) srow_chunk[threadIdx.x - kEpiThread0] = (out_row && amount) ? fold_t / p.chunk_tokens : -1;
         // pushed rows become visible to the peer through the releasing
         // thread's system-scope fence in nb_contributed (cumulative over the
         // CTA's stores ordered before it by the barrier) -- one fence per CTA

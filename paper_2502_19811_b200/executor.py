@@ -181,6 +181,7 @@ class LayerKnobs:
     stream_fuse: Optional[bool] = None
     sequential: Optional[bool] = None
     streamk: Optional[bool] = None
+    fold_stride: Optional[int] = None
 
     @classmethod
     def for_world(cls, world: int, **options) -> "LayerKnobs":

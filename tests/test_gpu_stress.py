@@ -6,10 +6,10 @@ this GPU), routing skew, an activation, combine weights or none, and kernel
 knobs (dispatch CTAs, pair groups, split-K slices, split-tail halves, one or
 two launches, stream-K tails) -- the paths the layer kernel can take: narrow
 last n-blocks, split-K with 2..8 slices and chunk helpers, fold chains up to
-top-8, layer1 halves, the per-n-block H gating.  Every case must match the
-reference within the stated tolerance and be bitwise identical when run
-twice (deterministic reductions and folds).  Seeded: a failure names its
-case.
+top-8 (one folder, or chained folds of stride 2/3/8), layer1 halves, the
+per-n-block H gating.  Every case must match the reference within the
+stated tolerance and be bitwise identical when run twice (deterministic
+reductions and folds).  Seeded: a failure names its case.
 """
 
 import os
@@ -43,7 +43,8 @@ def _case(seed):
                  fused=bool(r.integers(0, 4) > 0), streamk=bool(r.integers(0, 4) == 0),
                  wave1=int(r.choice([1, 2, 4, 8])), chunk_rows=int(r.choice([0, 1, 7, 16, 32])),
                  dedup=int(r.integers(0, 4) == 0), fold_order=bool(r.integers(0, 3) == 0),
-                 pull_local=bool(r.integers(0, 4) > 0), group1=int(r.choice([0, 0, 1, 4])))
+                 pull_local=bool(r.integers(0, 4) > 0), group1=int(r.choice([0, 0, 1, 4])),
+                 fold_stride=int(r.choice([0, 2, 2, 3, 8])))
     return E, topk, tp, ep, N, K, M, std, act, weighted, knobs
 
 
