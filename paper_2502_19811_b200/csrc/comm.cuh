@@ -285,19 +285,54 @@ __device__ void dispatch_rows(const LayerArgs& p, uint8_t* smem) {
 
 // Dedup (a7: one read per (token, rank)): the row of token t that pulls it is
 // its hosted row in the earliest-claimed tile (ties: lower slot); the smem
-// copy is bulk-stored to every hosted row of t.
-__device__ __forceinline__ bool primary_row(const LayerArgs& p, int t, int pos) {
-  const int K = p.topk;
-  const int my_q = p.claim_of_tile[pos >> 7];
+// copy is bulk-stored to every hosted row of t.  One lane per row computes
+// the row's job: whether it is the primary row and, if so, the destinations
+// (padded row, claim tile, the tile's rows).  The loads are issued level by
+// level over all top-k slots (tok_pos, then claim_of_tile, then the pair
+// table) -- three dependent round trips per batch of 32 rows instead of a
+// chain of ~3 per slot, which had made the loader's descriptor math, not the
+// copies, set the dedup dispatch rate (QW EP=8: 112 vs 40 us).
+__device__ __forceinline__ int dedup_job(const LayerArgs& p, int t, int pos, int4 (&dst)[8]) {
+  const int K = p.topk;  // <= 8 (host-checked)
+  int dpos[8], dq[8];
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2) dpos[s2] = s2 < K ? p.tok_pos[t * K + s2] : -1;
   const int my_s = p.row_widx[pos] - t * K;
-  for (int s2 = 0; s2 < K; ++s2) {
-    if (s2 == my_s) continue;
-    const int pos2 = p.tok_pos[t * K + s2];
-    if (pos2 < 0) continue;
-    const int q2 = p.claim_of_tile[pos2 >> 7];
-    if (q2 < my_q || (q2 == my_q && s2 < my_s)) return false;
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2) dq[s2] = dpos[s2] >= 0 ? p.claim_of_tile[dpos[s2] >> 7] : 0;
+  int my_q = 0;
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2)
+    if (s2 == my_s) my_q = dq[s2];
+  bool prim = true;
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2)
+    if (s2 != my_s && dpos[s2] >= 0 && (dq[s2] < my_q || (dq[s2] == my_q && s2 < my_s))) prim = false;
+  if (!prim) return -1;
+  int4 pr[8];
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2)
+    if (dpos[s2] >= 0) pr[s2] = reinterpret_cast<const int4*>(p.pairs)[dq[s2] >> 1];
+  int nd = 0;
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2) {
+    if (dpos[s2] < 0) continue;
+    // remote_rows() of claim tile dq: its populated rows (pull_local) or the
+    // remote suffix of the expert block
+    const int h = dq[s2] & 1;
+    const int base = pr[s2].y + kTileRows * h;
+    const int rows = max(0, min(kTileRows, pr[s2].z - kTileRows * h));
+    int nrd = rows;
+    if (!p.pull_local) {
+      const int rel = base - p.pad_off[pr[s2].x];
+      nrd = rows - min(rows, max(0, p.n_local[pr[s2].x] - rel));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j == nd) dst[j] = make_int4(dpos[s2], dq[s2], nrd, 0);
+    ++nd;
   }
-  return true;
+  return nd;
 }
 
 // layer0 dispatch, deduplicated per token (used by the zero-copy single-GPU
@@ -313,7 +348,6 @@ __device__ void dispatch_rows_dedup(const LayerArgs& p, uint8_t* smem) {
   const int n_comm = gridDim.x - p.n_compute;
   const int cid = blockIdx.x - p.n_compute;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = p.topk;
   if (warp == 0) {
     uint64_t ready_mask = 1ull << p.rank;
     int k = 0;
@@ -321,21 +355,12 @@ __device__ void dispatch_rows_dedup(const LayerArgs& p, uint8_t* smem) {
       const int n = re - rb;
       const int pos = padrow0 + rb + lane;
       const int t = lane < n ? p.gather_row[pos] : 0;
-      const bool prim = lane < n && primary_row(p, t, pos);
+      int4 dst[8];
+      int nd = lane < n ? dedup_job(p, t, pos, dst) : -1;
+      const bool prim = nd >= 0;
       const unsigned pm = __ballot_sync(0xffffffffu, prim);
       const int src = src_rank_of(t, p.M, p.world);
-      int nd = 0;
-      int4 dst[8];
-      if (prim)
-        for (int s2 = 0; s2 < K; ++s2) {
-          const int d = p.tok_pos[t * K + s2];
-          if (d >= 0) {
-            const int qd = p.claim_of_tile[d >> 7];
-            int pr0, nrd;
-            remote_rows(p, qd, pr0, nrd);
-            dst[nd++] = make_int4(d, qd, nrd, 0);
-          }
-        }
+      nd = max(nd, 0);
       int jj = k;  // job index of this lane's row
       for (int i = 0; i < lane; ++i) jj += (pm >> i) & 1;
       for (int i = 0; i < n; ++i) {
