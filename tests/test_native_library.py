@@ -57,3 +57,19 @@ def test_no_device_raises_loudly(monkeypatch):
         pytest.skip("GPU present")
     with pytest.raises(_lib.NativeUnavailable):
         _lib.require_device()
+
+
+def test_option_table_matches_the_header():
+    """_lib.OPTIONS (the names LayerKnobs / set_option use) is exactly the
+    header's COMET_OPT_* table, and LayerKnobs has a field per option."""
+    from paper_2502_19811_b200 import LayerKnobs
+    with open(os.path.join(ROOT, "include", "comet_b200.h")) as fh:
+        text = fh.read()
+    defs = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"#define COMET_OPT_([A-Z0-9_]+) (-?\d+)", text)}
+    count = defs.pop("count")
+    defs.pop("default", None)
+    assert defs == _lib.OPTIONS
+    assert sorted(defs.values()) == list(range(count))
+    fields = set(LayerKnobs.__dataclass_fields__)
+    assert set(_lib.OPTIONS) <= fields, set(_lib.OPTIONS) - fields
+    assert set(LayerKnobs().options()) == set(_lib.OPTIONS)
