@@ -405,6 +405,24 @@ def test_dispatch_dedup_bitwise(E, topk, tp, ep, M):
     assert_close(outs[1], ref, what=f"dedup E={E} topk={topk} tp={tp} ep={ep}")
 
 
+@pytest.mark.parametrize("E,topk,tp,ep,M", [(8, 2, 1, 8, 2048), (16, 4, 2, 2, 3000), (64, 8, 1, 8, 1500)])
+def test_dispatch_item_rows_bitwise(E, topk, tp, ep, M):
+    """The dispatch item size (COMET_OPT_CHUNK_ROWS: 0 = auto, ~one item per
+    dispatch CTA; 1..32 fixed; with and without per-token dedup) only changes
+    which CTA copies which rows: the result is bitwise the same."""
+    model = ModelConfig(L=1, E=E, topk=topk, N=512, K=1024)
+    par = ParallelSpec(tp, ep)
+    routing = build_routing(model, par, WorkloadSpec(M=M, seed=91, std=0.032))
+    w = random_weights(model, seed=92)
+    x = np.random.default_rng(93).standard_normal((M, 512))
+    cw = np.random.default_rng(94).random((M, topk))
+    outs = [run_emulated(x, w, routing, par, activation="silu", combine_weights=cw,
+                         knobs=LayerKnobs(n_comm0=16, n_comm1=0, chunk_rows=cr, dedup=dd)).cpu().numpy()
+            for cr, dd in ((0, 0), (1, 0), (5, 0), (32, 0), (0, 1), (8, 1))]
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+
+
 @pytest.mark.parametrize("act", ["gelu_tanh", "relu", None])
 def test_zerocopy_unweighted_activations(act):
     """Zero-copy host forward without combine weights (plain sum over the
