@@ -440,9 +440,6 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       const int NB = p.n_blocks;
       const int4 pr = reinterpret_cast<const int4*>(p.pairs)[w.pair];
       const int row0 = pr.y + kTileRows * static_cast<int>(cta);
-      wait(tfull, it & 1);
-      ptx::tc_fence_after();
-      const uint64_t t_e = ptx::globaltimer();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
       const int col0 = w.half > 0 ? static_cast<int>(kHalfN) : 0;  // half unit: its columns
       const int cols_left = p.out_ld - w.nb * kBlockN - col0;      // ragged last n-block (e.g. K/tp = 3200)
@@ -509,6 +506,30 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
           }
         }
       }
+#ifndef COMET_NO_FOLD_PREFETCH
+      // Fold rows were written by earlier units, up to a whole layer ago, and
+      // the weight stream has since evicted most of them from L2: the
+      // epilogue's register-limited loads (two rows in flight) then pay HBM
+      // round trips (QW top-8 folders: ~35 us epilogues at the launch tail).
+      // Pull this unit's column range of every fold row into L2 now, while
+      // the MMAs still run: one bulk prefetch per (lane, fold row), the
+      // quadrant's two warps taking alternate rows.  L2 is the coherence
+      // point, so a prefetch that lands before a predecessor's stores is
+      // harmless (the stores update the line; fold_wait orders the loads).
+      if (fold_t >= 0 && cols_left > 0) {
+        const int pcols = min(cols_left, n_chunks * 64);
+#pragma unroll
+        for (int j = 0; j < kMaxFold; ++j) {
+          if (j >= nf) break;
+          if ((j & 1) == sub)
+            ptx::bulk_prefetch_l2(p.yrows + static_cast<long long>(fpos[j]) * p.n_embed + w.nb * kBlockN + col0,
+                                  static_cast<uint32_t>(pcols) * 2u);
+        }
+      }
+#endif
+      wait(tfull, it & 1);
+      ptx::tc_fence_after();
+      const uint64_t t_e = ptx::globaltimer();
       // the rows this one folds live in units claimed before this one (same
       // n-block columns, lower sequence index): wait for their tiles
       auto fold_wait = [&]() {

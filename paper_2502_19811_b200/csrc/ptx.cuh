@@ -148,6 +148,13 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
 
+// Bulk L2 prefetch of `bytes` (multiple of 16, 16 B aligned) at `src`: no
+// registers, no smem, no completion -- later plain loads of the range hit L2.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
+}
+
 // 2D tile load; completion bytes land on `bar` of this CTA.
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar,
                                             int32_t c0, int32_t c1, uint64_t hint) {
