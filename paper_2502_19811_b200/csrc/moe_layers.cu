@@ -127,7 +127,7 @@ __device__ __forceinline__ void fold_regs(uint32_t (&acc)[32], const uint4* r, f
 }
 constexpr int kMaxFold = 7;  // earlier hosted rows of a token (top-k <= 8)
 #ifndef COMET_HELP_POLL_NS
-#define COMET_HELP_POLL_NS 3000
+#define COMET_HELP_POLL_NS 8000
 #endif
 constexpr uint64_t kHelpPollNs = COMET_HELP_POLL_NS;  // split-K: how long an earlier slice polls for the last one
 
