@@ -19,7 +19,7 @@ routing = build_routing(model, par, WorkloadSpec(M=M, seed=0))
 g0 = int(os.environ.get("G0", 8))
 nc = int(os.environ.get("NC0", 32))
 layer = MoELayer(model, par, 0, M, rank_weights_random(model, par, 0, torch.device("cuda", 0)),
-                 knobs=LayerKnobs(n_comm0=nc, group0=g0))
+                 knobs=LayerKnobs(n_comm0=nc, group0=g0, zc_order=int(os.environ.get("ZC_ORDER", 0)) or None))
 x_host = torch.randn(M, N).to(torch.bfloat16).pin_memory()
 ex_host = torch.from_numpy(routing.as_array().copy()).pin_memory()
 y_host = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
