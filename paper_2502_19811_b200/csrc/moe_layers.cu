@@ -550,7 +550,10 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
       // coalesced stores
       // contiguous destination rows (H, or yrows without the fused combine):
       // TMA tensor stores; fused-combine units write scattered token rows
-      const bool tma_out = (w.layer == 0 || !p.fuse_combine) && !COMET_DBG(p.debug, 16384);
+      // (fused combine: a warp none of whose 32 rows writes a token's final
+      // sum keeps its rows in yrows -- contiguous, so TMA stores too)
+      const bool tma_out = (w.layer == 0 || !p.fuse_combine || !__any_sync(0xffffffffu, out_row))
+                           && !COMET_DBG(p.debug, 16384);
       auto process = [&](int s, int seq, uint32_t (&v0)[32], uint32_t (&v1)[32]) {
         if (w.layer == 1) {  // no activation on FC2; fused combine: weight + earlier rows
 #pragma unroll
@@ -871,7 +874,9 @@ __device__ __forceinline__ void compute_role(const KernelArgs& f, uint8_t* smem,
         // pushed rows become visible to the peer through the releasing
         // thread's system-scope fence in nb_contributed (cumulative over the
         // CTA's stores ordered before it by the barrier) -- one fence per CTA
-        // instead of one per thread
+        // instead of one per thread; rows written by TMA stores (completed
+        // above) are ordered before the release by a proxy fence, as in layer0
+        if (tma_out) ptx::fence_async_global();
         ptx::named_bar_sync(1, kEpiThreads);
         if (p.out_cnt && p.fuse_combine && threadIdx.x == kEpiThread0 && amount) {
           // streamed forward: these output rows' halves are final -> count
